@@ -1,0 +1,121 @@
+/* libpmg_cuda.so -- the B200 (sm_100a) solve path of the PCG + V(1,1)-cycle
+ * multigrid method for multi-patch IgA, behind a plain C ABI.
+ *
+ * Every entry point replaces one call of the reference's Backend concept
+ * (the seam consumed by mg_cycle_generic / mg_precondition / pcg_generic,
+ * /root/reference/proj/include/patchmg/multigrid.hpp:120-189), implemented by
+ * SerialBackend (multigrid.hpp:80-114) and ParallelBackend
+ * (parallel.hpp:267-341, parallel.cpp:247-468).
+ *
+ * Vector representation.  A pmg_vec holds one value per patch-lattice slot
+ * (num_patches x (n+p)^dim, patch-major, axis 0 fastest), i.e. the paper's
+ * accumulated (Type I) / distributed (Type II) vectors applied per patch:
+ *   accumulated: every replica of a global dof holds its global value;
+ *   distributed: the replicas' values sum to the global value.
+ * Dirichlet slots hold 0.  Whether a vector is read as accumulated or
+ * distributed is fixed by the operation, exactly as the reference's AccVec /
+ * DistVec types fix it; pmg_vec_upload/download take the form explicitly.
+ *
+ * Errors: every function returns a PMG_* status (pmg_types.h) that maps 1:1
+ * onto the reference exception classes; pmg_last_error() holds the message.
+ * No function falls back to a CPU implementation.
+ */
+#ifndef PMG_CUDA_H
+#define PMG_CUDA_H
+
+#include "pmg_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pmg_ctx pmg_ctx;
+typedef struct pmg_vec pmg_vec;
+
+enum { PMG_ACCUMULATED = 0, PMG_DISTRIBUTED = 1 };
+
+/* Multi-GPU placement: this context owns patches [patch_begin, patch_end) of
+ * the hierarchy (contiguous_partition, parallel.cpp:181-198).  nccl_comm is an
+ * ncclComm_t spanning `size` ranks (one GPU each) or NULL when size == 1. */
+typedef struct {
+  int rank;
+  int size;
+  int patch_begin;
+  int patch_end;
+  void* nccl_comm;
+} pmg_comm_desc;
+
+/* Upload one hierarchy (Hierarchy, multigrid.hpp:42-75) to `device`.
+ * comm == NULL: single GPU owning every patch. */
+int pmg_ctx_create(const pmg_hierarchy_desc* desc, int device, const pmg_comm_desc* comm, pmg_ctx** out);
+void pmg_ctx_destroy(pmg_ctx* ctx);
+/* Message of the last failure on ctx (or of the last failed create when NULL). */
+const char* pmg_last_error(pmg_ctx* ctx);
+/* what: 0 finest level, 1 lattice slots of level `level`, 2 device bytes held,
+ *       3 num_dofs of level `level`, 4 local patches.  level = what >> 8. */
+int pmg_ctx_info(pmg_ctx* ctx, int what, int64_t* out);
+/* Launch everything on this cudaStream_t from now on (NULL: the ctx stream). */
+int pmg_set_stream(pmg_ctx* ctx, void* stream);
+int pmg_synchronize(pmg_ctx* ctx);
+
+/* Vectors (AccumulatedVector / DistributedVector, parallel.hpp:169-260). */
+int pmg_vec_create(pmg_ctx* ctx, int level, pmg_vec** out);
+void pmg_vec_free(pmg_vec* v);
+/* global host vector (num_dofs) <-> lattice vector in the given form;
+ * to_accumulated / to_distributed_owner / gather_global(_sum),
+ * parallel.cpp:428-468 */
+int pmg_vec_upload(pmg_ctx* ctx, pmg_vec* v, int form, const double* host, int64_t n);
+int pmg_vec_download(pmg_ctx* ctx, pmg_vec* v, int form, double* host, int64_t n);
+/* raw lattice copies (num local patches x (n+p)^dim) */
+int pmg_vec_lattice_upload(pmg_ctx* ctx, pmg_vec* v, const double* host, int64_t n);
+int pmg_vec_lattice_download(pmg_ctx* ctx, pmg_vec* v, double* host, int64_t n);
+int pmg_vec_zero(pmg_ctx* ctx, pmg_vec* v);                  /* zero_acc */
+int pmg_vec_copy(pmg_ctx* ctx, const pmg_vec* src, pmg_vec* dst);
+
+/* Backend operations. */
+/* apply_op: out(dist) = A u(acc)                 multigrid.hpp:93, parallel.cpp:281-300 */
+int pmg_apply_op(pmg_ctx* ctx, int level, const pmg_vec* u, pmg_vec* out);
+/* residual: out(dist) = f(dist) - A u(acc)       multigrid.hpp:94-96, parallel.cpp:302-304 */
+int pmg_residual(pmg_ctx* ctx, int level, const pmg_vec* f, const pmg_vec* u, pmg_vec* out);
+/* accumulate: interface sum Sigma               multigrid.hpp:97, parallel.cpp:306-337 */
+int pmg_accumulate(pmg_ctx* ctx, int level, const pmg_vec* r, pmg_vec* out);
+/* smooth: out(acc) = sum_T P_T L_T^-1 P_T^T r    multigrid.hpp:99, parallel.cpp:353-355 */
+int pmg_smooth(pmg_ctx* ctx, int level, const pmg_vec* r, pmg_vec* out);
+/* restrict_residual: level -> level-1 (dist)    multigrid.hpp:100-102, parallel.cpp:357-382 */
+int pmg_restrict(pmg_ctx* ctx, int level, const pmg_vec* r, pmg_vec* out_coarse);
+/* add_prolonged: u += c P coarse (acc)          multigrid.hpp:103-105, parallel.cpp:384-409 */
+int pmg_add_prolonged(pmg_ctx* ctx, int level, const pmg_vec* coarse, double c, pmg_vec* u);
+/* coarse_solve: out(acc) = A0^-1 r(dist)        multigrid.hpp:106, parallel.cpp:411-422 */
+int pmg_coarse_solve(pmg_ctx* ctx, const pmg_vec* r, pmg_vec* out);
+/* dot(dist, acc), globally reduced             multigrid.hpp:107, parallel.cpp:424-426 */
+int pmg_dot(pmg_ctx* ctx, int level, const pmg_vec* a, const pmg_vec* b, double* out);
+/* axpy_acc / axpy_dist: y += a x                 multigrid.hpp:108-109 */
+int pmg_axpy(pmg_ctx* ctx, double a, const pmg_vec* x, pmg_vec* y);
+/* xpay_acc: p = z + beta p                       multigrid.hpp:110 */
+int pmg_xpay(pmg_ctx* ctx, const pmg_vec* z, double beta, pmg_vec* p);
+
+/* Fused paths. */
+/* mg_cycle_generic at `level`, in place on u(acc), f(dist)   multigrid.hpp:120-141 */
+int pmg_mg_cycle(pmg_ctx* ctx, int level, pmg_vec* u, const pmg_vec* f);
+/* mg_precondition: z(acc) = one cycle from zero on r(dist)   multigrid.hpp:144-149 */
+int pmg_precondition(pmg_ctx* ctx, const pmg_vec* r, pmg_vec* z);
+/* pcg_generic with the V-cycle preconditioner on device-resident vectors;
+ * history has room for max_iter+1 norms; PMG_ERR_DIVERGENCE at the cap
+ * (multigrid.hpp:155-189, multigrid.cpp:72-89). */
+int pmg_pcg_solve_device(pmg_ctx* ctx, const pmg_vec* f, double tol, int max_iter, pmg_vec* u, double* history,
+                         int* iterations);
+/* The same from host memory: f_host is the global load vector (num_dofs of the
+ * finest level), u_host receives the global solution -- the pcg_solve call of
+ * the reference (multigrid.hpp:196-197) end to end, copies included. */
+int pmg_pcg_solve(pmg_ctx* ctx, const double* f_host, int64_t n, double tol, int max_iter, double* u_host,
+                  double* history, int* iterations);
+
+/* Instrumentation: which = 0 kernel launches since ctx creation (count);
+ * which = 1 launches of the band SpMV; which = 2 reset counters. */
+int pmg_kernel_stats(pmg_ctx* ctx, int which, int64_t* count, double* reserved);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PMG_CUDA_H */

@@ -1,0 +1,81 @@
+"""Build the native libraries in-tree.
+
+  paper_1804_02539_b200/lib/libpmg_host.so  hierarchy builder (g++)
+  paper_1804_02539_b200/lib/libpmg_cuda.so  sm_100a kernels + C ABI (nvcc)
+  oracle/_build/liboracle.so                CPU parity oracle (g++), test-only
+
+The .so files are git-ignored but travel to the GPU box with the snapshot.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+LIB = PKG / "lib"
+ORACLE_BUILD = ROOT / "oracle" / "_build"
+
+HOST_SRC = sorted((PKG / "csrc" / "host").glob("*.cpp"))
+CUDA_SRC = sorted((PKG / "csrc" / "cuda").glob("*.cu"))
+ORACLE_SRC = [ROOT / "oracle" / "oracle.cpp"]
+
+CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-shared", "-pthread", "-ffp-contract=off", "-Wall"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+NVCCFLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-lineinfo", "-O3", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills",
+    "-I" + str(ROOT / "include"),
+]
+
+
+def _stale(out: Path, srcs) -> bool:
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    deps = list(srcs)
+    for d in (PKG / "csrc", ROOT / "include", ROOT / "oracle"):
+        deps += list(d.rglob("*.h")) + list(d.rglob("*.hpp")) + list(d.rglob("*.cuh"))
+    return any(Path(s).stat().st_mtime > t for s in deps)
+
+
+def _run(cmd):
+    print(" ".join(str(c) for c in cmd), flush=True)
+    subprocess.run([str(c) for c in cmd], check=True)
+
+
+def build_host(force: bool = False) -> Path:
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "libpmg_host.so"
+    if force or _stale(out, HOST_SRC):
+        _run(["g++", *CXXFLAGS, "-o", out, *HOST_SRC])
+    return out
+
+
+def build_oracle(force: bool = False) -> Path:
+    ORACLE_BUILD.mkdir(parents=True, exist_ok=True)
+    out = ORACLE_BUILD / "liboracle.so"
+    if force or _stale(out, ORACLE_SRC):
+        _run(["g++", *CXXFLAGS, "-o", out, *ORACLE_SRC])
+    return out
+
+
+def build_cuda(force: bool = False) -> Path:
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "libpmg_cuda.so"
+    if CUDA_SRC and (force or _stale(out, CUDA_SRC)):
+        _run([NVCC, *NVCCFLAGS, "-o", out, *CUDA_SRC, "-ldl"])
+    return out
+
+
+def build_all(force: bool = False) -> None:
+    build_host(force)
+    build_oracle(force)
+    build_cuda(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)

@@ -1,0 +1,1078 @@
+// libpmg_cuda: context creation (host-side layout planning + uploads), the C
+// ABI of include/pmg_cuda.h, and the device-resident V-cycle / PCG drivers.
+//
+// The drivers restate, on device-resident lattice vectors:
+//   mg_cycle_generic / mg_precondition / pcg_generic  multigrid.hpp:120-189
+// with the Backend operations of SerialBackend (multigrid.hpp:80-114) /
+// ParallelBackend (parallel.cpp:247-468) implemented by the kernels in
+// kernels_*.cu.  Two reference operations are restated exactly and cheaper:
+//   * the first residual of a cycle from a zero start is f itself
+//     (f - A*0 == f bitwise), so that SpMV is skipped;
+//   * restriction runs on the distributed per-patch shares directly; the
+//     owner masking of restrict_full (transfer.cpp:68-91) only picks one split
+//     of the same sum, and P^T is linear.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../../include/pmg_cuda.h"
+#include "internal.cuh"
+
+using namespace pmgcu;
+
+namespace {
+
+struct PmgError : std::runtime_error {
+  int code;
+  PmgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw PmgError(PMG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DevLevel {
+  int n = 0, ext = 0, O = 0, K = 0;
+  long long S = 0, lat_n = 0, N = 0;
+  double* band = nullptr;
+  int* l2g = nullptr;
+  unsigned char* owner = nullptr;
+  int* rep_off = nullptr;
+  int* rep_slot = nullptr;
+  int* goff = nullptr;
+  int* gslot = nullptr;
+  int ngroups = 0;
+  // interior FD
+  FdPiece* d_int = nullptr;
+  int n_int = 0;
+  bool int_wide = false;
+  int2* int_items[6] = {};
+  int n_int_items[6] = {};
+  // faces
+  FdPiece* d_face = nullptr;
+  int n_face = 0;
+  bool face_wide = false;
+  int* face_dof_g = nullptr;
+  long long face_ndof = 0;
+  int2* face_items[4] = {};
+  int n_face_items[4] = {};
+  // edges / vertices
+  EdgePiece* d_edges = nullptr;
+  int n_edges = 0;
+  int* edge_dof_g = nullptr;
+  int* vert_g = nullptr;
+  double* vert_scalar = nullptr;
+  int n_verts = 0;
+  // two-scale factor from level-1 (level >= 1)
+  TsDev ts{};
+  // V-cycle workspace
+  double* f = nullptr;
+  double* u = nullptr;
+  double* r = nullptr;
+};
+
+}  // namespace
+
+struct pmg_ctx {
+  int device = 0;
+  int dim = 0, degree = 0, K_global = 0, pb = 0, pe = 0, nl = 0;
+  pmg_cycle_params prm{};
+  std::vector<DevLevel> lv;
+  double* work[2] = {nullptr, nullptr};
+  double* tbuf[2] = {nullptr, nullptr};
+  double* face_buf[2] = {nullptr, nullptr};
+  double* Ainv = nullptr;
+  int n0 = 0;
+  double* coarse_rhs = nullptr;
+  double* coarse_x = nullptr;
+  double* partial = nullptr;
+  int partial_n = 0;
+  double* scal = nullptr;     // device scalars
+  double* h_scal = nullptr;   // pinned mirror
+  double* staging = nullptr;  // device global-vector staging (finest num_dofs)
+  long long staging_n = 0;
+  // PCG vectors on the finest level
+  double *pcg_r = nullptr, *pcg_z = nullptr, *pcg_p = nullptr, *pcg_Ap = nullptr, *pcg_acc = nullptr,
+         *pcg_u = nullptr, *pcg_f = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+  long long launches = 0, spmv_launches = 0;
+  std::string err;
+
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    allocs.push_back(p);
+    bytes += count * sizeof(T);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const T* h, size_t count) {
+    T* d = alloc<T>(count);
+    if (count) ck(cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    return d;
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    return upload(v.data(), v.size());
+  }
+  ~pmg_ctx() {
+    cudaSetDevice(device);
+    for (void* p : allocs) cudaFree(p);
+    if (h_scal) cudaFreeHost(h_scal);
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+};
+
+struct pmg_vec {
+  pmg_ctx* ctx;
+  int level;
+  double* d;
+  long long n;
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+// Explicit inverse of the banded Cholesky operator: column j is the
+// reference BandedCholesky::solve (banded.cpp:61-77) of e_j; stored row-major.
+std::vector<double> banded_inverse(int n, int bw, const double* l) {
+  const int w = bw + 1;
+  std::vector<double> inv(size_t(n) * n), y(n);
+  for (int j = 0; j < n; ++j) {
+    for (int i = 0; i < n; ++i) {
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int k = std::max(0, i - bw); k < i; ++k) s -= l[size_t(i) * w + (i - k)] * y[k];
+      y[i] = s / l[size_t(i) * w];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < std::min(n, i + bw + 1); ++k) s -= l[size_t(k) * w + (k - i)] * y[k];
+      y[i] = s / l[size_t(i) * w];
+    }
+    for (int i = 0; i < n; ++i) inv[size_t(i) * n + j] = y[i];
+  }
+  return inv;
+}
+
+// A0^-1 = L^-T L^-1 from the lower Cholesky factor (column-major); row-major out
+std::vector<double> spd_inverse(int n, const double* L) {
+  std::vector<double> Li(size_t(n) * n, 0.0);  // column-major lower inverse
+  for (int j = 0; j < n; ++j) {
+    Li[size_t(j) * n + j] = 1.0 / L[size_t(j) * n + j];
+    for (int i = j + 1; i < n; ++i) {
+      double s = 0.0;
+      for (int k = j; k < i; ++k) s += L[size_t(k) * n + i] * Li[size_t(j) * n + k];
+      Li[size_t(j) * n + i] = -s / L[size_t(i) * n + i];
+    }
+  }
+  std::vector<double> inv(size_t(n) * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = 0.0;
+      for (int k = i; k < n; ++k) s += Li[size_t(i) * n + k] * Li[size_t(j) * n + k];
+      inv[size_t(i) * n + j] = inv[size_t(j) * n + i] = s;
+    }
+  return inv;
+}
+
+void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
+  const pmg_level_desc& ld = D.levels[l];
+  DevLevel& L = c.lv[l];
+  const int d = D.dim, p = D.degree;
+  L.n = ld.elements;
+  L.ext = ld.elements + p;
+  L.O = 1;
+  L.S = 1;
+  for (int a = 0; a < d; ++a) {
+    L.O *= 2 * p + 1;
+    L.S *= L.ext;
+  }
+  L.K = c.pe - c.pb;
+  L.lat_n = L.S * L.K;
+  L.N = ld.num_dofs;
+  const long long S = L.S;
+  const int* l2g_all = ld.l2g;
+  const int* l2g = l2g_all + (size_t)c.pb * S;
+
+  // ---- band
+  L.band = c.alloc<double>(size_t(L.K) * L.O * S);
+  if (ld.band_format == PMG_BAND_TENSOR) {
+    ck(cudaMemcpy(L.band, ld.band + (size_t)c.pb * L.O * S, sizeof(double) * size_t(L.K) * L.O * S,
+                  cudaMemcpyHostToDevice),
+       "band upload");
+  } else if (ld.band_format == PMG_BAND_CSR) {
+    // place every CSR entry at its tensor offset (PatchOperator, assembly.hpp:16-25)
+    std::vector<double> hb(size_t(L.O) * S);
+    const int W = 2 * p + 1;
+    for (int k = 0; k < L.K; ++k) {
+      std::fill(hb.begin(), hb.end(), 0.0);
+      const int64_t* rp = ld.csr_row_ptr[c.pb + k];
+      const int32_t* cols = ld.csr_cols[c.pb + k];
+      const double* vals = ld.csr_vals[c.pb + k];
+      for (long long r = 0; r < S; ++r)
+        for (int64_t q = rp[r]; q < rp[r + 1]; ++q) {
+          long long rr = r, cc = cols[q];
+          int o = 0, mul = 1;
+          for (int a = 0; a < d; ++a) {
+            const int delta = int(cc % L.ext) - int(rr % L.ext);
+            if (delta < -p || delta > p) throw PmgError(PMG_ERR_DOMAIN, "CSR column outside the tensor band");
+            o += (delta + p) * mul;
+            mul *= W;
+            rr /= L.ext;
+            cc /= L.ext;
+          }
+          hb[size_t(o) * S + r] += vals[q];
+        }
+      ck(cudaMemcpy(L.band + size_t(k) * L.O * S, hb.data(), sizeof(double) * hb.size(), cudaMemcpyHostToDevice),
+         "band upload");
+    }
+  } else {
+    throw PmgError(PMG_ERR_CONFIG, "unknown band format");
+  }
+  L.l2g = c.upload(l2g, size_t(L.lat_n));
+  launch_zero_dirichlet_band(c.stream, d, p, L.ext, S, L.K, L.l2g, L.band);
+
+  // ---- replicas: global owner patch over all patches; local replica CSR
+  std::vector<int> owner_patch(size_t(L.N), -1);
+  for (int k = 0; k < D.num_patches; ++k)
+    for (long long f = 0; f < S; ++f) {
+      const int g = l2g_all[size_t(k) * S + f];
+      if (g >= 0 && owner_patch[g] < 0) owner_patch[g] = k;
+    }
+  std::vector<int> rep_off(size_t(L.N) + 1, 0);
+  for (long long s = 0; s < L.lat_n; ++s)
+    if (l2g[s] >= 0) rep_off[l2g[s] + 1]++;
+  for (long long g = 0; g < L.N; ++g) rep_off[g + 1] += rep_off[g];
+  std::vector<int> rep_slot(rep_off.back()), cur(rep_off.begin(), rep_off.end() - 1);
+  std::vector<unsigned char> owner(size_t(L.lat_n), 0);
+  for (long long s = 0; s < L.lat_n; ++s) {
+    const int g = l2g[s];
+    if (g < 0) continue;
+    rep_slot[cur[g]++] = int(s);
+    if (owner_patch[g] == c.pb + int(s / S)) owner[s] = 1;
+  }
+  L.rep_off = c.upload(rep_off);
+  L.rep_slot = c.upload(rep_slot);
+  L.owner = c.upload(owner);
+  std::vector<int> goff(1, 0), gslot;
+  for (long long g = 0; g < L.N; ++g)
+    if (rep_off[g + 1] - rep_off[g] >= 2) {
+      for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) gslot.push_back(rep_slot[q]);
+      goff.push_back(int(gslot.size()));
+    }
+  L.ngroups = int(goff.size()) - 1;
+  L.goff = c.upload(goff);
+  L.gslot = c.upload(gslot);
+
+  // ---- pieces
+  std::map<const double*, std::pair<const double*, const double*>> vmats;  // V -> (Bfwd, Bbwd)
+  auto mats_of = [&](const double* V, int m) {
+    auto it = vmats.find(V);
+    if (it != vmats.end()) return it->second;
+    std::vector<double> bf(size_t(m) * m);
+    for (int k = 0; k < m; ++k)
+      for (int n = 0; n < m; ++n) bf[size_t(k) * m + n] = V[size_t(n) * m + k];
+    const double* dbf = c.upload(bf);
+    const double* dbb = c.upload(V, size_t(m) * m);
+    return vmats[V] = {dbf, dbb};
+  };
+  std::map<const double*, const double*> diags;
+  auto diag_of = [&](const double* h, long long n) {
+    auto it = diags.find(h);
+    if (it != diags.end()) return it->second;
+    return diags[h] = c.upload(h, size_t(n));
+  };
+  std::map<std::vector<double>, const double*> linvs;
+  std::vector<FdPiece> h_int, h_face;
+  std::vector<int> face_dofs, edge_dofs, vert_g;
+  std::vector<double> vert_scalar;
+  std::vector<EdgePiece> h_edges;
+  long long work_int = 0, work_face = 0;
+  int maxdim_int = 0, maxdim_face = 0;
+  for (int i = 0; i < ld.num_pieces; ++i) {
+    const pmg_piece_desc& pc = ld.pieces[i];
+    // pieces of other ranks' patches are skipped; interface pieces touching
+    // this rank are kept (every replica here takes part in the sum)
+    bool mine = false;
+    for (int64_t q = 0; q < pc.ndofs && !mine; ++q) {
+      const int g = pc.dofs[q];
+      if (rep_off[g + 1] > rep_off[g]) mine = true;
+    }
+    if (!mine) continue;
+    if (pc.kind == PMG_PIECE_INTERIOR) {
+      if (pc.naxes != d) throw PmgError(PMG_ERR_DOMAIN, "interior piece: axis count mismatch");
+      const int k = pc.patch - c.pb;
+      // locate the box: the first dof's lattice position is the corner
+      const int g0 = pc.dofs[0];
+      int slot0 = -1;
+      for (int q = rep_off[g0]; q < rep_off[g0 + 1]; ++q)
+        if (rep_slot[q] / S == k) slot0 = rep_slot[q];
+      if (slot0 < 0) throw PmgError(PMG_ERR_DOMAIN, "interior piece: corner dof not on its patch");
+      const long long local0 = slot0 - (long long)k * S;
+      int lo[3] = {0, 0, 0};
+      long long rem = local0;
+      for (int a = 0; a < d; ++a) {
+        lo[a] = int(rem % L.ext);
+        rem /= L.ext;
+      }
+      FdPiece fp{};
+      fp.naxes = d;
+      fp.total = 1;
+      for (int a = 0; a < d; ++a) {
+        fp.dims[a] = pc.dims[a];
+        fp.total *= pc.dims[a];
+        if (lo[a] + pc.dims[a] > L.ext) throw PmgError(PMG_ERR_DOMAIN, "interior piece box leaves the lattice");
+        maxdim_int = std::max(maxdim_int, pc.dims[a]);
+      }
+      if (fp.total != pc.ndofs) throw PmgError(PMG_ERR_DOMAIN, "piece smoother: local vector size mismatch");
+      // every dof of the box must be the lattice slot in box order (classify_dofs, topology.cpp:408-436)
+      {
+        int idx[3] = {0, 0, 0};
+        for (long long q = 0; q < fp.total; ++q) {
+          long long loc = 0;
+          for (int a = d - 1; a >= 0; --a) loc = loc * L.ext + (lo[a] + idx[a]);
+          if (l2g[(long long)k * S + loc] != pc.dofs[q])
+            throw PmgError(PMG_ERR_DOMAIN, "interior piece is not a lattice box");
+          for (int a = 0; a < d; ++a) {
+            if (++idx[a] < pc.dims[a]) break;
+            idx[a] = 0;
+          }
+        }
+      }
+      fp.ext = L.ext;
+      fp.lat_base = slot0;
+      fp.work_off = work_int;
+      work_int += fp.total;
+      for (int a = 0; a < d; ++a) {
+        auto m = mats_of(pc.V[a], pc.dims[a]);
+        fp.B[a][0] = m.first;
+        fp.B[a][1] = m.second;
+      }
+      fp.diag = diag_of(pc.diag, fp.total);
+      h_int.push_back(fp);
+    } else if (pc.kind == PMG_PIECE_FACE) {
+      FdPiece fp{};
+      fp.naxes = 2;
+      fp.total = 1;
+      for (int a = 0; a < 2; ++a) {
+        fp.dims[a] = pc.dims[a];
+        fp.total *= pc.dims[a];
+        maxdim_face = std::max(maxdim_face, pc.dims[a]);
+        auto m = mats_of(pc.V[a], pc.dims[a]);
+        fp.B[a][0] = m.first;
+        fp.B[a][1] = m.second;
+      }
+      if (fp.total != pc.ndofs) throw PmgError(PMG_ERR_DOMAIN, "piece smoother: local vector size mismatch");
+      fp.dims[2] = 1;
+      fp.work_off = work_face;
+      work_face += fp.total;
+      fp.diag = diag_of(pc.diag, fp.total);
+      for (int64_t q = 0; q < pc.ndofs; ++q) face_dofs.push_back(pc.dofs[q]);
+      h_face.push_back(fp);
+    } else if (pc.kind == PMG_PIECE_EDGE) {
+      if (pc.chol_dim != pc.ndofs) throw PmgError(PMG_ERR_DOMAIN, "piece smoother: local vector size mismatch");
+      if (pc.ndofs > 512) throw PmgError(PMG_ERR_CONFIG, "edge pieces longer than 512 dofs are not supported");
+      std::vector<double> key(pc.chol_l, pc.chol_l + size_t(pc.chol_dim) * (pc.chol_bw + 1));
+      key.push_back(pc.chol_dim);
+      key.push_back(pc.chol_bw);
+      auto it = linvs.find(key);
+      const double* dinv;
+      if (it != linvs.end()) {
+        dinv = it->second;
+      } else {
+        dinv = c.upload(banded_inverse(pc.chol_dim, pc.chol_bw, pc.chol_l));
+        linvs[key] = dinv;
+      }
+      h_edges.push_back(EdgePiece{int(pc.ndofs), (long long)edge_dofs.size(), dinv});
+      for (int64_t q = 0; q < pc.ndofs; ++q) edge_dofs.push_back(pc.dofs[q]);
+    } else {
+      vert_g.push_back(pc.dofs[0]);
+      vert_scalar.push_back(pc.scalar);
+    }
+  }
+  if (maxdim_int > 288 || maxdim_face > 288)
+    throw PmgError(PMG_ERR_CONFIG, "fast-diagonalization pieces wider than 288 dofs per axis are not supported");
+  L.int_wide = maxdim_int > 72;
+  L.face_wide = maxdim_face > 72;
+  L.n_int = int(h_int.size());
+  L.d_int = c.upload(h_int);
+  L.n_face = int(h_face.size());
+  L.d_face = c.upload(h_face);
+  L.face_dof_g = c.upload(face_dofs);
+  L.face_ndof = (long long)face_dofs.size();
+  L.n_edges = int(h_edges.size());
+  L.d_edges = c.upload(h_edges);
+  L.edge_dof_g = c.upload(edge_dofs);
+  L.n_verts = int(vert_g.size());
+  L.vert_g = c.upload(vert_g);
+  L.vert_scalar = c.upload(vert_scalar);
+  auto make_items = [&](const std::vector<FdPiece>& ps, int naxes, bool wide, int2** items, int* counts) {
+    const int BM = fd_rows_per_block(wide);
+    for (int pass = 0; pass < 2 * naxes; ++pass) {
+      std::vector<int2> it;
+      for (int i = 0; i < int(ps.size()); ++i) {
+        const long long R = ps[i].total / ps[i].dims[pass % naxes];
+        for (long long r0 = 0; r0 < R; r0 += BM) it.push_back(make_int2(i, int(r0)));
+      }
+      counts[pass] = int(it.size());
+      items[pass] = c.upload(it);
+    }
+  };
+  make_items(h_int, d, L.int_wide, L.int_items, L.n_int_items);
+  if (d == 3) make_items(h_face, 2, L.face_wide, L.face_items, L.n_face_items);
+
+  // ---- two-scale factor (TransferOperator ctor, transfer.cpp:10-19)
+  if (l >= 1) {
+    const int nf = ld.ts_fine_dim, ncd = ld.ts_coarse_dim;
+    int nnz = 0;
+    for (int i = 0; i < nf; ++i) nnz = std::max(nnz, ld.ts_row_off[i] + ld.ts_row_len[i]);
+    L.ts.fine_dim = nf;
+    L.ts.coarse_dim = ncd;
+    L.ts.row_start = c.upload(ld.ts_row_start, nf);
+    L.ts.row_len = c.upload(ld.ts_row_len, nf);
+    L.ts.row_off = c.upload(ld.ts_row_off, nf);
+    L.ts.vals = c.upload(ld.ts_vals, size_t(nnz));
+    std::vector<int> col_off(size_t(ncd) + 1, 0), col_row;
+    std::vector<double> col_val;
+    std::vector<std::vector<std::pair<int, double>>> cols(ncd);
+    for (int i = 0; i < nf; ++i)
+      for (int q = 0; q < ld.ts_row_len[i]; ++q)
+        cols[ld.ts_row_start[i] + q].push_back({i, ld.ts_vals[ld.ts_row_off[i] + q]});
+    for (int j = 0; j < ncd; ++j) {
+      for (auto& e : cols[j]) {
+        col_row.push_back(e.first);
+        col_val.push_back(e.second);
+      }
+      col_off[j + 1] = int(col_row.size());
+    }
+    L.ts.col_off = c.upload(col_off);
+    L.ts.col_row = c.upload(col_row);
+    L.ts.col_val = c.upload(col_val);
+    if (nf != L.ext) throw PmgError(PMG_ERR_DOMAIN, "transfer: fine level must have twice the elements");
+  }
+  L.f = c.alloc<double>(size_t(L.lat_n));
+  L.u = c.alloc<double>(size_t(L.lat_n));
+  L.r = c.alloc<double>(size_t(L.lat_n));
+  ck(cudaMemset(L.f, 0, sizeof(double) * L.lat_n), "memset");
+  ck(cudaMemset(L.u, 0, sizeof(double) * L.lat_n), "memset");
+  ck(cudaMemset(L.r, 0, sizeof(double) * L.lat_n), "memset");
+}
+
+void build_ctx(pmg_ctx& c, const pmg_hierarchy_desc& D) {
+  c.dim = D.dim;
+  c.degree = D.degree;
+  c.K_global = D.num_patches;
+  c.nl = D.num_levels;
+  c.prm = D.params;
+  if (D.dim < 2 || D.dim > 3) throw PmgError(PMG_ERR_CONFIG, "dimension must be 2 or 3");
+  if (D.num_levels < 2) throw PmgError(PMG_ERR_CONFIG, "need at least one refinement level");
+  if (D.params.nu < 1 || D.params.mu < 1 || D.params.mu > 2) throw PmgError(PMG_ERR_CONFIG, "bad cycle parameters");
+  c.lv.resize(c.nl);
+  fd_configure();
+  size_t work_n = 1, tbuf_n = 1, face_n = 1;
+  for (int l = 0; l < c.nl; ++l) {
+    build_level(c, D, l);
+    const pmg_level_desc& ld = D.levels[l];
+    long long wi = 0, wf = 0;
+    for (int i = 0; i < ld.num_pieces; ++i) {
+      const pmg_piece_desc& pc = ld.pieces[i];
+      if (pc.kind == PMG_PIECE_INTERIOR) wi += pc.ndofs;
+      if (pc.kind == PMG_PIECE_FACE) wf += pc.ndofs;
+    }
+    work_n = std::max(work_n, size_t(std::max(wi, wf)));
+    face_n = std::max(face_n, size_t(wf));
+    if (l >= 1) {  // largest intermediate of the tensor transfer: ext_c * ext_f^(d-1) per patch
+      long long t = c.lv[l - 1].ext;
+      for (int a = 1; a < c.dim; ++a) t *= c.lv[l].ext;
+      tbuf_n = std::max(tbuf_n, size_t(t * c.lv[l].K));
+      tbuf_n = std::max(tbuf_n, size_t(c.lv[l].lat_n));
+    }
+  }
+  c.work[0] = c.alloc<double>(work_n);
+  c.work[1] = c.alloc<double>(work_n);
+  c.face_buf[0] = c.alloc<double>(face_n);
+  c.face_buf[1] = c.alloc<double>(face_n);
+  c.tbuf[0] = c.alloc<double>(tbuf_n);
+  c.tbuf[1] = c.alloc<double>(tbuf_n);
+  // coarse solve (Hierarchy::coarse_solve): explicit inverse for a GEMV
+  c.n0 = D.coarse_n;
+  if (c.n0 != c.lv[0].N) throw PmgError(PMG_ERR_DOMAIN, "coarse matrix size does not match level 0");
+  c.Ainv = c.upload(spd_inverse(c.n0, D.coarse_L));
+  c.coarse_rhs = c.alloc<double>(size_t(c.n0));
+  c.coarse_x = c.alloc<double>(size_t(c.n0));
+  long long maxlat = 0;
+  for (auto& L : c.lv) maxlat = std::max(maxlat, L.lat_n);
+  c.partial_n = std::max(spmv_blocks(maxlat), dot_blocks(maxlat));
+  c.partial = c.alloc<double>(size_t(c.partial_n));
+  c.scal = c.alloc<double>(16);
+  ck(cudaMemset(c.scal, 0, 16 * sizeof(double)), "memset");
+  ck(cudaMallocHost(&c.h_scal, 16 * sizeof(double)), "cudaMallocHost");
+  const DevLevel& F = c.lv.back();
+  c.staging_n = std::max<long long>(F.N, 1);
+  c.staging = c.alloc<double>(size_t(c.staging_n));
+  for (double** v : {&c.pcg_r, &c.pcg_z, &c.pcg_p, &c.pcg_Ap, &c.pcg_acc, &c.pcg_u, &c.pcg_f}) {
+    *v = c.alloc<double>(size_t(F.lat_n));
+    ck(cudaMemset(*v, 0, sizeof(double) * F.lat_n), "memset");
+  }
+  ck(cudaStreamSynchronize(c.stream), "build sync");
+  ck(cudaGetLastError(), "build kernels");
+}
+
+// ================================================================ operations
+// All launch on c.stream and count their kernels.
+
+void op_spmv(pmg_ctx& c, int l, const double* x, const double* f, double* y, double* dot_partial = nullptr) {
+  const DevLevel& L = c.lv[l];
+  SpmvArgs a{c.dim, c.degree, L.ext, L.S, L.K, L.band, x, f, y, dot_partial};
+  launch_spmv(c.stream, a);
+  c.launches++;
+  c.spmv_launches++;
+}
+
+// smooth: interior FD, faces, edges + vertices.  out_mode SET: out = alpha z
+// on every piece slot; ADD: out += alpha z.
+void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double alpha) {
+  const DevLevel& L = c.lv[l];
+  const int d = c.dim;
+  const int np = 2 * d;
+  for (int pass = 0; pass < np; ++pass) {
+    const int in_mode = pass == 0 ? FD_IN_LATTICE : FD_IN_WORK;
+    int out_mode = FD_OUT_WORK;
+    if (pass == d - 1) out_mode = FD_OUT_WORK_DIAG;
+    if (pass == np - 1) out_mode = add ? FD_OUT_LATTICE_ADD : FD_OUT_LATTICE_SET;
+    launch_fd_pass(c.stream, L.int_wide, L.d_int, L.int_items[pass], L.n_int_items[pass], pass, d, in_mode, out_mode,
+                   r, out, alpha, c.work[(pass + 1) & 1], c.work[pass & 1]);
+    if (L.n_int_items[pass]) c.launches++;
+  }
+  if (d == 3 && L.n_face > 0) {
+    launch_gather_sum(c.stream, L.face_dof_g, L.face_ndof, L.rep_off, L.rep_slot, r, c.face_buf[1]);
+    c.launches++;
+    for (int pass = 0; pass < 4; ++pass) {
+      const int out_mode = pass == 1 ? FD_OUT_WORK_DIAG : FD_OUT_WORK;
+      launch_fd_pass(c.stream, L.face_wide, L.d_face, L.face_items[pass], L.n_face_items[pass], pass, 2, FD_IN_WORK,
+                     out_mode, nullptr, nullptr, 0.0, c.face_buf[(pass + 1) & 1], c.face_buf[pass & 1]);
+      c.launches++;
+    }
+    launch_scatter(c.stream, L.face_dof_g, L.face_ndof, L.rep_off, L.rep_slot, c.face_buf[1], out, add ? 1 : 0, alpha);
+    c.launches++;
+  }
+  if (L.n_edges + L.n_verts > 0) {
+    launch_edges_vertices(c.stream, L.d_edges, L.n_edges, L.edge_dof_g, L.vert_g, L.vert_scalar, L.n_verts, L.rep_off,
+                          L.rep_slot, r, out, add ? 1 : 0, alpha);
+    c.launches++;
+  }
+}
+
+// restriction level l -> l-1 on distributed shares; out coarse (dist)
+void op_restrict(pmg_ctx& c, int l, const double* r, double* out) {
+  const DevLevel& F = c.lv[l];
+  const DevLevel& C = c.lv[l - 1];
+  int dims[3] = {F.ext, F.ext, F.ext};
+  const double* src = r;
+  for (int a = 0; a < c.dim; ++a) {
+    double* dst = (a == c.dim - 1) ? out : c.tbuf[a & 1];
+    launch_ts_axis(c.stream, F.ts, true, F.K, c.dim, dims, a, src, dst);
+    c.launches++;
+    dims[a] = C.ext;
+    src = dst;
+  }
+  launch_mask_dirichlet(c.stream, C.l2g, C.lat_n, out);
+  c.launches++;
+}
+
+// u(level l) += coef * P coarse(level l-1)
+void op_prolong_add(pmg_ctx& c, int l, const double* coarse, double coef, double* u) {
+  const DevLevel& F = c.lv[l];
+  const DevLevel& C = c.lv[l - 1];
+  int dims[3] = {C.ext, C.ext, C.ext};
+  const double* src = coarse;
+  for (int a = 0; a < c.dim; ++a) {
+    double* dst = c.tbuf[a & 1];
+    launch_ts_axis(c.stream, F.ts, false, F.K, c.dim, dims, a, src, dst);
+    c.launches++;
+    dims[a] = F.ext;
+    src = dst;
+  }
+  launch_masked_axpy(c.stream, F.l2g, F.lat_n, coef, src, u);
+  c.launches++;
+}
+
+void op_coarse(pmg_ctx& c, const double* r, double* out) {
+  const DevLevel& L = c.lv[0];
+  launch_coarse(c.stream, L.rep_off, L.rep_slot, L.l2g, c.n0, L.lat_n, c.Ainv, r, c.coarse_rhs, c.coarse_x, out);
+  c.launches += c.n0 > 0 ? 3 : 1;
+}
+
+// dot(dist a, acc b) into device scalar slot
+void op_dot(pmg_ctx& c, int l, const double* a, const double* b, double* dst) {
+  const DevLevel& L = c.lv[l];
+  launch_dot_partial(c.stream, a, b, L.lat_n, c.partial);
+  launch_sum_partials(c.stream, c.partial, dot_blocks(L.lat_n), dst);
+  c.launches += 2;
+}
+
+void op_accumulate(pmg_ctx& c, int l, const double* r, double* out) {
+  const DevLevel& L = c.lv[l];
+  if (out != r) {
+    launch_copy(c.stream, r, out, L.lat_n);
+    c.launches++;
+  }
+  launch_group_sum(c.stream, L.goff, L.gslot, L.ngroups, r == out ? out : r, out);
+  if (L.ngroups) c.launches++;
+}
+
+// mg_cycle_generic (multigrid.hpp:120-141) on the ctx workspace.
+// `zero` marks u == 0 on entry (every recursive call and mg_precondition).
+void cycle(pmg_ctx& c, int l, double* u, const double* f, bool zero) {
+  DevLevel& L = c.lv[l];
+  const double tau = c.prm.tau;
+  for (int i = 0; i < c.prm.nu; ++i) {
+    if (zero && i == 0) {
+      op_smooth(c, l, f, u, false, tau);  // u = 0 + tau L^-1 (f - A 0)
+    } else {
+      op_spmv(c, l, u, f, L.r);
+      op_smooth(c, l, L.r, u, true, tau);
+    }
+  }
+  op_spmv(c, l, u, f, L.r);
+  DevLevel& C = c.lv[l - 1];
+  op_restrict(c, l, L.r, C.f);
+  if (l == 1) {
+    op_coarse(c, C.f, C.u);
+  } else {
+    for (int i = 0; i < c.prm.mu; ++i) cycle(c, l - 1, C.u, C.f, i == 0);
+  }
+  op_prolong_add(c, l, C.u, c.prm.damp_coarse ? tau : 1.0, u);
+  for (int i = 0; i < c.prm.nu; ++i) {
+    op_spmv(c, l, u, f, L.r);
+    op_smooth(c, l, L.r, u, true, tau);
+  }
+}
+
+void precondition(pmg_ctx& c, const double* r, double* z) {
+  // z starts as zero: every piece slot is written by the first smooth (SET),
+  // Dirichlet slots of z are never written and stay 0
+  cycle(c, c.nl - 1, z, r, true);
+}
+
+void sync_check(pmg_ctx& c) {
+  ck(cudaStreamSynchronize(c.stream), "stream sync");
+  ck(cudaGetLastError(), "kernel launch");
+}
+
+// pcg_generic (multigrid.hpp:155-189) on device-resident vectors f, u.
+int pcg_device(pmg_ctx& c, const double* f, double tol, int max_iter, double* u, double* history, int* iters) {
+  const int Lf = c.nl - 1;
+  const DevLevel& F = c.lv[Lf];
+  const long long n = F.lat_n;
+  double* r = c.pcg_r;
+  double* z = c.pcg_z;
+  double* p = c.pcg_p;
+  double* Ap = c.pcg_Ap;
+  double* racc = c.pcg_acc;
+  double* s = c.scal;
+  launch_fill(c.stream, u, n, 0.0);
+  launch_copy(c.stream, f, r, n);
+  c.launches += 2;
+  auto norm2 = [&]() {  // sqrt(dot(r, accumulate(r)))
+    op_accumulate(c, Lf, r, racc);
+    op_dot(c, Lf, r, racc, s + 5);
+    launch_pcg_scalars(c.stream, 2, s);
+    c.launches++;
+  };
+  auto read_scalars = [&]() {
+    ck(cudaMemcpyAsync(c.h_scal, s, 8 * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "scalar D2H");
+    sync_check(c);
+  };
+  norm2();
+  read_scalars();
+  const double r0 = c.h_scal[6];
+  history[0] = r0;
+  *iters = 0;
+  if (r0 == 0.0) return PMG_OK;
+  launch_fill(c.stream, z, n, 0.0);
+  c.launches++;
+  precondition(c, r, z);
+  launch_copy(c.stream, z, p, n);
+  c.launches++;
+  op_dot(c, Lf, r, z, s + 0);  // rz
+  for (int k = 1; k <= max_iter; ++k) {
+    op_spmv(c, Lf, p, nullptr, Ap, c.partial);  // Ap and the partials of Ap.p
+    launch_sum_partials(c.stream, c.partial, spmv_blocks(n), s + 1);
+    launch_pcg_scalars(c.stream, 0, s);  // alpha = rz / pAp
+    launch_axpy(c.stream, 0.0, s + 2, 1.0, p, u, n);
+    launch_axpy(c.stream, 0.0, s + 2, -1.0, Ap, r, n);
+    c.launches += 4;
+    norm2();
+    read_scalars();
+    if (c.h_scal[7] != 0.0) {
+      c.h_scal[7] = 0.0;
+      ck(cudaMemsetAsync(s + 7, 0, sizeof(double), c.stream), "memset");
+      throw PmgError(PMG_ERR_DEFINITENESS, "pcg: search direction with nonpositive energy");
+    }
+    const double rn = c.h_scal[6];
+    history[k] = rn;
+    *iters = k;
+    if (rn <= tol * r0) return PMG_OK;
+    precondition(c, r, z);
+    op_dot(c, Lf, r, z, s + 3);          // rz_next
+    launch_pcg_scalars(c.stream, 1, s);  // beta, rz = rz_next
+    launch_xpay(c.stream, z, 0.0, s + 4, p, n);
+    c.launches += 2;
+  }
+  return PMG_ERR_DIVERGENCE;
+}
+
+template <class F>
+int guarded(pmg_ctx* c, F&& f) {
+  try {
+    if (c) ck(cudaSetDevice(c->device), "cudaSetDevice");
+    f();
+    return PMG_OK;
+  } catch (const PmgError& e) {
+    if (c) c->err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return PMG_ERR_GENERIC;
+  }
+}
+
+void need(bool ok, int code, const char* msg) {
+  if (!ok) throw PmgError(code, msg);
+}
+
+void check_vec(const pmg_ctx* c, const pmg_vec* v, int level) {
+  need(v != nullptr && v->ctx == c, PMG_ERR_DOMAIN, "vector belongs to another context");
+  need(v->level == level, PMG_ERR_DOMAIN, "vector level mismatch");
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+const char* pmg_last_error(pmg_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
+
+int pmg_ctx_create(const pmg_hierarchy_desc* desc, int device, const pmg_comm_desc* comm, pmg_ctx** out) {
+  if (!desc || !out) {
+    g_create_error = "pmg_ctx_create: null argument";
+    return PMG_ERR_CONFIG;
+  }
+  *out = nullptr;
+  auto c = std::make_unique<pmg_ctx>();
+  c->device = device;
+  c->pb = 0;
+  c->pe = desc->num_patches;
+  try {
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    need(device >= 0 && device < ndev, PMG_ERR_CONFIG, "device index out of range");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    if (comm) {
+      need(comm->size >= 1 && comm->rank >= 0 && comm->rank < comm->size, PMG_ERR_CONFIG, "bad rank description");
+      need(comm->patch_begin >= 0 && comm->patch_end <= desc->num_patches && comm->patch_begin < comm->patch_end,
+           PMG_ERR_CONFIG, "bad patch range");
+      need(comm->size == 1, PMG_ERR_CONFIG, "multi-rank contexts need the exchange layer (pmg_comm_desc.size > 1)");
+      c->pb = comm->patch_begin;
+      c->pe = comm->patch_end;
+    }
+    ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->stream = c->own_stream;
+    build_ctx(*c, *desc);
+  } catch (const PmgError& e) {
+    g_create_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    return PMG_ERR_GENERIC;
+  }
+  *out = c.release();
+  return PMG_OK;
+}
+
+void pmg_ctx_destroy(pmg_ctx* ctx) { delete ctx; }
+
+int pmg_ctx_info(pmg_ctx* ctx, int what, int64_t* out) {
+  return guarded(ctx, [&] {
+    const int level = what >> 8;
+    const int w = what & 0xff;
+    need(level >= 0 && level < ctx->nl, PMG_ERR_DOMAIN, "level out of range");
+    switch (w) {
+      case 0: *out = ctx->nl - 1; break;
+      case 1: *out = ctx->lv[level].lat_n; break;
+      case 2: *out = int64_t(ctx->bytes); break;
+      case 3: *out = ctx->lv[level].N; break;
+      case 4: *out = ctx->pe - ctx->pb; break;
+      default: throw PmgError(PMG_ERR_CONFIG, "unknown info query");
+    }
+  });
+}
+
+int pmg_set_stream(pmg_ctx* ctx, void* stream) {
+  return guarded(ctx, [&] { ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream; });
+}
+
+int pmg_synchronize(pmg_ctx* ctx) {
+  return guarded(ctx, [&] { sync_check(*ctx); });
+}
+
+int pmg_vec_create(pmg_ctx* ctx, int level, pmg_vec** out) {
+  return guarded(ctx, [&] {
+    need(level >= 0 && level < ctx->nl, PMG_ERR_DOMAIN, "level out of range");
+    auto v = std::make_unique<pmg_vec>();
+    v->ctx = ctx;
+    v->level = level;
+    v->n = ctx->lv[level].lat_n;
+    ck(cudaMalloc(&v->d, sizeof(double) * std::max<long long>(v->n, 1)), "cudaMalloc vec");
+    ck(cudaMemset(v->d, 0, sizeof(double) * v->n), "memset vec");
+    *out = v.release();
+  });
+}
+
+void pmg_vec_free(pmg_vec* v) {
+  if (!v) return;
+  cudaSetDevice(v->ctx->device);
+  cudaFree(v->d);
+  delete v;
+}
+
+int pmg_vec_upload(pmg_ctx* ctx, pmg_vec* v, int form, const double* host, int64_t n) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, v, v ? v->level : 0);
+    const DevLevel& L = ctx->lv[v->level];
+    need(n == L.N, PMG_ERR_DOMAIN, "global vector size mismatch");
+    need(L.N <= ctx->staging_n, PMG_ERR_DOMAIN, "staging too small");
+    ck(cudaMemcpyAsync(ctx->staging, host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    launch_lattice_from_global(ctx->stream, L.l2g, L.owner, L.lat_n, form == PMG_DISTRIBUTED ? 1 : 0, ctx->staging,
+                               v->d);
+    ctx->launches++;
+    sync_check(*ctx);
+  });
+}
+
+int pmg_vec_download(pmg_ctx* ctx, pmg_vec* v, int form, double* host, int64_t n) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, v, v ? v->level : 0);
+    const DevLevel& L = ctx->lv[v->level];
+    need(n == L.N, PMG_ERR_DOMAIN, "global vector size mismatch");
+    launch_global_from_lattice(ctx->stream, L.rep_off, L.rep_slot, L.N, form == PMG_DISTRIBUTED ? 1 : 0, v->d,
+                               ctx->staging);
+    ctx->launches++;
+    ck(cudaMemcpyAsync(host, ctx->staging, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    sync_check(*ctx);
+  });
+}
+
+int pmg_vec_lattice_upload(pmg_ctx* ctx, pmg_vec* v, const double* host, int64_t n) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, v, v ? v->level : 0);
+    need(n == v->n, PMG_ERR_DOMAIN, "lattice size mismatch");
+    ck(cudaMemcpyAsync(v->d, host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    sync_check(*ctx);
+  });
+}
+
+int pmg_vec_lattice_download(pmg_ctx* ctx, pmg_vec* v, double* host, int64_t n) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, v, v ? v->level : 0);
+    need(n == v->n, PMG_ERR_DOMAIN, "lattice size mismatch");
+    ck(cudaMemcpyAsync(host, v->d, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    sync_check(*ctx);
+  });
+}
+
+int pmg_vec_zero(pmg_ctx* ctx, pmg_vec* v) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, v, v ? v->level : 0);
+    launch_fill(ctx->stream, v->d, v->n, 0.0);
+    ctx->launches++;
+  });
+}
+
+int pmg_vec_copy(pmg_ctx* ctx, const pmg_vec* src, pmg_vec* dst) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, src, src ? src->level : 0);
+    check_vec(ctx, dst, src->level);
+    launch_copy(ctx->stream, src->d, dst->d, src->n);
+    ctx->launches++;
+  });
+}
+
+int pmg_apply_op(pmg_ctx* ctx, int level, const pmg_vec* u, pmg_vec* out) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, u, level);
+    check_vec(ctx, out, level);
+    op_spmv(*ctx, level, u->d, nullptr, out->d);
+  });
+}
+
+int pmg_residual(pmg_ctx* ctx, int level, const pmg_vec* f, const pmg_vec* u, pmg_vec* out) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, f, level);
+    check_vec(ctx, u, level);
+    check_vec(ctx, out, level);
+    op_spmv(*ctx, level, u->d, f->d, out->d);
+  });
+}
+
+int pmg_accumulate(pmg_ctx* ctx, int level, const pmg_vec* r, pmg_vec* out) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, r, level);
+    check_vec(ctx, out, level);
+    op_accumulate(*ctx, level, r->d, out->d);
+  });
+}
+
+int pmg_smooth(pmg_ctx* ctx, int level, const pmg_vec* r, pmg_vec* out) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, r, level);
+    check_vec(ctx, out, level);
+    need(r->d != out->d, PMG_ERR_DOMAIN, "smooth: input and output must differ");
+    launch_fill(ctx->stream, out->d, out->n, 0.0);
+    ctx->launches++;
+    op_smooth(*ctx, level, r->d, out->d, false, 1.0);
+  });
+}
+
+int pmg_restrict(pmg_ctx* ctx, int level, const pmg_vec* r, pmg_vec* out) {
+  return guarded(ctx, [&] {
+    need(level >= 1 && level < ctx->nl, PMG_ERR_DOMAIN, "restrict: level out of range");
+    check_vec(ctx, r, level);
+    check_vec(ctx, out, level - 1);
+    op_restrict(*ctx, level, r->d, out->d);
+  });
+}
+
+int pmg_add_prolonged(pmg_ctx* ctx, int level, const pmg_vec* coarse, double coef, pmg_vec* u) {
+  return guarded(ctx, [&] {
+    need(level >= 1 && level < ctx->nl, PMG_ERR_DOMAIN, "prolong: level out of range");
+    check_vec(ctx, coarse, level - 1);
+    check_vec(ctx, u, level);
+    op_prolong_add(*ctx, level, coarse->d, coef, u->d);
+  });
+}
+
+int pmg_coarse_solve(pmg_ctx* ctx, const pmg_vec* r, pmg_vec* out) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, r, 0);
+    check_vec(ctx, out, 0);
+    op_coarse(*ctx, r->d, out->d);
+  });
+}
+
+int pmg_dot(pmg_ctx* ctx, int level, const pmg_vec* a, const pmg_vec* b, double* out) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, a, level);
+    check_vec(ctx, b, level);
+    op_dot(*ctx, level, a->d, b->d, ctx->scal + 8);
+    ck(cudaMemcpyAsync(ctx->h_scal + 8, ctx->scal + 8, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    sync_check(*ctx);
+    *out = ctx->h_scal[8];
+  });
+}
+
+int pmg_axpy(pmg_ctx* ctx, double a, const pmg_vec* x, pmg_vec* y) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, x, x ? x->level : 0);
+    check_vec(ctx, y, x->level);
+    launch_axpy(ctx->stream, a, nullptr, 1.0, x->d, y->d, x->n);
+    ctx->launches++;
+  });
+}
+
+int pmg_xpay(pmg_ctx* ctx, const pmg_vec* z, double beta, pmg_vec* p) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, z, z ? z->level : 0);
+    check_vec(ctx, p, z->level);
+    launch_xpay(ctx->stream, z->d, beta, nullptr, p->d, z->n);
+    ctx->launches++;
+  });
+}
+
+int pmg_mg_cycle(pmg_ctx* ctx, int level, pmg_vec* u, const pmg_vec* f) {
+  return guarded(ctx, [&] {
+    need(level >= 1 && level < ctx->nl, PMG_ERR_DOMAIN, "cycle: level out of range");
+    check_vec(ctx, u, level);
+    check_vec(ctx, f, level);
+    cycle(*ctx, level, u->d, f->d, false);
+  });
+}
+
+int pmg_precondition(pmg_ctx* ctx, const pmg_vec* r, pmg_vec* z) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, r, ctx->nl - 1);
+    check_vec(ctx, z, ctx->nl - 1);
+    need(r->d != z->d, PMG_ERR_DOMAIN, "precondition: input and output must differ");
+    launch_fill(ctx->stream, z->d, z->n, 0.0);
+    ctx->launches++;
+    precondition(*ctx, r->d, z->d);
+  });
+}
+
+int pmg_pcg_solve_device(pmg_ctx* ctx, const pmg_vec* f, double tol, int max_iter, pmg_vec* u, double* history,
+                         int* iterations) {
+  int rc = PMG_OK;
+  int g = guarded(ctx, [&] {
+    check_vec(ctx, f, ctx->nl - 1);
+    check_vec(ctx, u, ctx->nl - 1);
+    need(max_iter >= 1, PMG_ERR_CONFIG, "max-iter: must be positive");
+    rc = pcg_device(*ctx, f->d, tol, max_iter, u->d, history, iterations);
+    sync_check(*ctx);
+  });
+  if (g != PMG_OK) return g;
+  if (rc == PMG_ERR_DIVERGENCE) ctx->err = "pcg: no convergence within the iteration limit";
+  return rc;
+}
+
+int pmg_pcg_solve(pmg_ctx* ctx, const double* f_host, int64_t n, double tol, int max_iter, double* u_host,
+                  double* history, int* iterations) {
+  int rc = PMG_OK;
+  int g = guarded(ctx, [&] {
+    const DevLevel& F = ctx->lv.back();
+    need(n == F.N, PMG_ERR_DOMAIN, "global vector size mismatch");
+    need(max_iter >= 1, PMG_ERR_CONFIG, "max-iter: must be positive");
+    ck(cudaMemcpyAsync(ctx->staging, f_host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    launch_lattice_from_global(ctx->stream, F.l2g, F.owner, F.lat_n, 1, ctx->staging, ctx->pcg_f);
+    ctx->launches++;
+    rc = pcg_device(*ctx, ctx->pcg_f, tol, max_iter, ctx->pcg_u, history, iterations);
+    launch_global_from_lattice(ctx->stream, F.rep_off, F.rep_slot, F.N, 0, ctx->pcg_u, ctx->staging);
+    ctx->launches++;
+    ck(cudaMemcpyAsync(u_host, ctx->staging, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    sync_check(*ctx);
+  });
+  if (g != PMG_OK) return g;
+  if (rc == PMG_ERR_DIVERGENCE) ctx->err = "pcg: no convergence within the iteration limit";
+  return rc;
+}
+
+int pmg_kernel_stats(pmg_ctx* ctx, int which, int64_t* count, double* reserved) {
+  (void)reserved;
+  return guarded(ctx, [&] {
+    switch (which) {
+      case 0: *count = ctx->launches; break;
+      case 1: *count = ctx->spmv_launches; break;
+      case 2:
+        ctx->launches = ctx->spmv_launches = 0;
+        if (count) *count = 0;
+        break;
+      default: throw PmgError(PMG_ERR_CONFIG, "unknown stats query");
+    }
+  });
+}
+
+}  // extern "C"

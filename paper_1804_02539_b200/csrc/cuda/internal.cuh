@@ -1,0 +1,117 @@
+// Internal device data layout and kernel launchers of libpmg_cuda.
+//
+// HBM layout (one context = the patches one GPU owns):
+//   lattice vectors   double[K][S], S = (n+p)^d, patch-major, axis 0 fastest
+//   band              double[K][O][S], O = (2p+1)^d, offset-major: a warp's 32
+//                     consecutive rows read 256 contiguous bytes per offset;
+//                     Dirichlet rows and columns are zeroed at upload
+//   l2g               int32[K][S] (global dof or -1)
+//   replica CSR       per global dof, its lattice slots in ascending (patch,
+//                     local) order -- DofMapper::reps (topology.cpp:367-372)
+//   FD work buffers   per interior/face piece, its tensor box contiguous
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace pmgcu {
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------- FD
+struct FdPiece {
+  int dims[3];
+  int naxes;
+  long long total;
+  long long lat_base;  // slot of the box corner (interior pieces)
+  int ext;             // lattice extent (interior pieces)
+  long long work_off;  // offset in the work buffers
+  const double* B[3][2];  // [axis][0 fwd: B(k,n)=V(k,n) | 1 bwd: B(k,n)=V(n,k)], row-major k*N+n
+  const double* diag;     // total, original (axis 0 fastest) layout
+};
+
+enum FdIn { FD_IN_WORK = 0, FD_IN_LATTICE = 1 };
+enum FdOut { FD_OUT_WORK = 0, FD_OUT_WORK_DIAG = 1, FD_OUT_LATTICE_SET = 2, FD_OUT_LATTICE_ADD = 3 };
+
+// One fast-diagonalization pass (contract one axis, rotate the layout).
+// items: (piece, first row) per CTA; wide = true selects the N <= 288 tile.
+void launch_fd_pass(cudaStream_t s, bool wide, const FdPiece* pieces, const int2* items, int nitems, int pass,
+                    int naxes, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
+                    const double* work_in, double* work_out);
+int fd_rows_per_block(bool wide);
+void fd_configure();  // per device, before the first pass
+
+// ---------------------------------------------------------------- SpMV
+struct SpmvArgs {
+  int dim, degree, ext;
+  long long S;         // rows per patch
+  int K;               // patches
+  const double* band;  // [K][O][S]
+  const double* x;     // lattice vector (accumulated)
+  const double* f;     // residual mode: f (distributed); nullptr for y = A x
+  double* y;
+  double* dot_partial; // optional: per-block partial of sum y*x (nullptr: none)
+};
+void launch_spmv(cudaStream_t s, const SpmvArgs& a);
+int spmv_blocks(long long rows);
+
+// ---------------------------------------------------------------- misc kernels
+void launch_fill(cudaStream_t s, double* x, long long n, double v);
+void launch_copy(cudaStream_t s, const double* x, double* y, long long n);
+void launch_axpy(cudaStream_t s, double a, const double* a_dev, double sign, const double* x, double* y, long long n);
+void launch_xpay(cudaStream_t s, const double* z, double beta, const double* beta_dev, double* p, long long n);
+void launch_scale_set(cudaStream_t s, double a, const double* x, double* y, long long n);  // y = a x
+// deterministic dot: fixed grid -> partials -> one ordered final sum
+int dot_blocks(long long n);
+void launch_dot_partial(cudaStream_t s, const double* a, const double* b, long long n, double* partial);
+void launch_sum_partials(cudaStream_t s, const double* partial, int nparts, double* out);
+// Sigma: out = r, then every multi-replica dof gets the ordered sum written to all its replicas
+void launch_group_sum(cudaStream_t s, const int* goff, const int* gslot, int ngroups, const double* r, double* out);
+// gather-sum / scatter for interface piece dofs via the replica CSR of global dofs
+void launch_gather_sum(cudaStream_t s, const int* dof_g, long long ndof, const int* rep_off, const int* rep_slot,
+                       const double* r, double* buf);
+void launch_scatter(cudaStream_t s, const int* dof_g, long long ndof, const int* rep_off, const int* rep_slot,
+                    const double* buf, double* out, int add, double alpha);
+// edges (dense inverse GEMV) and vertices (scalar) in one launch
+struct EdgePiece {
+  int m;
+  long long dof_off;  // into the concatenated edge dof list
+  const double* Linv; // row-major m x m
+};
+void launch_edges_vertices(cudaStream_t s, const EdgePiece* edges, int nedges, const int* edge_dof_g,
+                           const int* vert_g, const double* vert_scalar, int nverts, const int* rep_off,
+                           const int* rep_slot, const double* r, double* out, int add, double alpha);
+// global <-> lattice
+void launch_lattice_from_global(cudaStream_t s, const int* l2g, const unsigned char* owner, long long n, int form,
+                                const double* g, double* lat);
+void launch_global_from_lattice(cudaStream_t s, const int* rep_off, const int* rep_slot, long long ndofs, int form,
+                                const double* lat, double* g);
+// coarse: rhs[g] = sum reps; x = Ainv rhs; out[slot] = x[l2g]
+void launch_coarse(cudaStream_t s, const int* rep_off, const int* rep_slot, const int* l2g, int n0, long long lat_n,
+                   const double* Ainv, const double* r, double* rhs, double* x, double* out);
+// two-scale passes
+struct TsDev {
+  int fine_dim, coarse_dim;
+  const int* row_start;  // [fine]
+  const int* row_len;
+  const int* row_off;
+  const double* vals;
+  const int* col_off;    // transpose CSR: [coarse+1]
+  const int* col_row;    // fine rows, ascending
+  const double* col_val;
+};
+// one tensor axis pass over K patches: in dims -> out dims (axis changes extent)
+void launch_ts_axis(cudaStream_t s, const TsDev& ts, bool transpose, int K, int d, const int* in_dims, int axis,
+                    const double* in, double* out);
+// final fine write of a prolongation: u[slot] += c * val where l2g >= 0
+void launch_masked_axpy(cudaStream_t s, const int* l2g, long long n, double c, const double* val, double* u);
+void launch_mask_dirichlet(cudaStream_t s, const int* l2g, long long n, double* v);
+void launch_zero_dirichlet_band(cudaStream_t s, int dim, int degree, int ext, long long S, int K, const int* l2g,
+                                double* band);
+// scalar helpers on device: out = num/den ; check energy
+void launch_pcg_scalars(cudaStream_t s, int op, double* scal);
+
+}  // namespace pmgcu

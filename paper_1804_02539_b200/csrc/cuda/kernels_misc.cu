@@ -1,0 +1,389 @@
+// Vector algebra, deterministic reductions, interface sums, interface-piece
+// solves, intergrid transfers and the coarse solve.
+//
+// All of these are HBM- or latency-bound.  Reductions use a fixed grid and a
+// fixed-order final sum, so every result is bitwise reproducible run to run
+// (the property the reference gets from ascending-rank sums, parallel.hpp:26-30).
+#include "internal.cuh"
+
+namespace pmgcu {
+
+namespace {
+
+inline int grid_for(long long n, int per_thread = 1) {
+  long long g = (n + (long long)kThreads * per_thread - 1) / ((long long)kThreads * per_thread);
+  return int(g < 1 ? 1 : g);
+}
+
+__global__ void fill_kernel(double* x, long long n, double v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    x[i] = v;
+}
+
+__global__ void copy_kernel(const double* __restrict__ x, double* __restrict__ y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = x[i];
+}
+
+// y += a x  (axpy_acc / axpy_dist, multigrid.hpp:108-109); a from device when given
+__global__ void axpy_kernel(double a, const double* a_dev, double sign, const double* __restrict__ x,
+                            double* __restrict__ y, long long n) {
+  const double s = a_dev ? sign * a_dev[0] : a;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] += s * x[i];
+}
+
+// p = z + beta p  (xpay_acc, multigrid.hpp:110)
+__global__ void xpay_kernel(const double* __restrict__ z, double beta, const double* beta_dev, double* __restrict__ p,
+                            long long n) {
+  const double b = beta_dev ? beta_dev[0] : beta;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = z[i] + b * p[i];
+}
+
+__global__ void scale_set_kernel(double a, const double* __restrict__ x, double* __restrict__ y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = a * x[i];
+}
+
+__device__ inline double block_sum(double v) {
+  __shared__ double red[kThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+  return s;
+}
+
+__global__ void dot_partial_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                                   double* __restrict__ partial) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kThreads)
+    s += a[i] * b[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void sum_partials_kernel(const double* __restrict__ partial, int n, double* out) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += kThreads) s += partial[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+// Sigma over multi-replica dofs: ordered sum written to every replica
+// (ParallelBackend::accumulate, parallel.cpp:306-337; serially the scatter-add
+// of MultiPatchOperator::apply, assembly.cpp:276-277)
+__global__ void group_sum_kernel(const int* __restrict__ goff, const int* __restrict__ gslot, int ngroups,
+                                 const double* __restrict__ r, double* __restrict__ out) {
+  const int g = blockIdx.x * kThreads + threadIdx.x;
+  if (g >= ngroups) return;
+  double s = 0.0;
+  for (int q = goff[g]; q < goff[g + 1]; ++q) s += r[gslot[q]];
+  for (int q = goff[g]; q < goff[g + 1]; ++q) out[gslot[q]] = s;
+}
+
+__global__ void gather_sum_kernel(const int* __restrict__ dof_g, long long ndof, const int* __restrict__ rep_off,
+                                  const int* __restrict__ rep_slot, const double* __restrict__ r,
+                                  double* __restrict__ buf) {
+  const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+  if (i >= ndof) return;
+  const int g = dof_g[i];
+  double s = 0.0;
+  for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) s += r[rep_slot[q]];
+  buf[i] = s;
+}
+
+__global__ void scatter_kernel(const int* __restrict__ dof_g, long long ndof, const int* __restrict__ rep_off,
+                               const int* __restrict__ rep_slot, const double* __restrict__ buf,
+                               double* __restrict__ out, int add, double alpha) {
+  const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+  if (i >= ndof) return;
+  const int g = dof_g[i];
+  const double v = buf[i];
+  for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) {
+    if (add)
+      out[rep_slot[q]] += alpha * v;
+    else
+      out[rep_slot[q]] = alpha * v;
+  }
+}
+
+// Edge pieces: z = L_T^-1 (sum of replica shares) with the explicit inverse of
+// the banded operator (BandedCholesky::solve, banded.cpp:61-77), one CTA per
+// edge; the trailing CTA handles every vertex piece (smoother.cpp:36-38).
+__global__ void __launch_bounds__(kThreads) edges_vertices_kernel(
+    const EdgePiece* __restrict__ edges, int nedges, const int* __restrict__ edge_dof_g,
+    const int* __restrict__ vert_g, const double* __restrict__ vert_scalar, int nverts,
+    const int* __restrict__ rep_off, const int* __restrict__ rep_slot, const double* __restrict__ r,
+    double* __restrict__ out, int add, double alpha) {
+  __shared__ double buf[512];
+  if (blockIdx.x < nedges) {
+    const EdgePiece e = edges[blockIdx.x];
+    const int* dofs = edge_dof_g + e.dof_off;
+    for (int i = threadIdx.x; i < e.m; i += kThreads) {
+      const int g = dofs[i];
+      double s = 0.0;
+      for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) s += r[rep_slot[q]];
+      buf[i] = s;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < e.m; i += kThreads) {
+      const double* row = e.Linv + (long long)i * e.m;
+      double z = 0.0;
+      for (int j = 0; j < e.m; ++j) z = fma(row[j], buf[j], z);
+      const int g = dofs[i];
+      for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) {
+        if (add)
+          out[rep_slot[q]] += alpha * z;
+        else
+          out[rep_slot[q]] = alpha * z;
+      }
+    }
+    return;
+  }
+  for (int v = threadIdx.x; v < nverts; v += kThreads) {
+    const int g = vert_g[v];
+    double s = 0.0;
+    for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) s += r[rep_slot[q]];
+    const double z = s / vert_scalar[v];
+    for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) {
+      if (add)
+        out[rep_slot[q]] += alpha * z;
+      else
+        out[rep_slot[q]] = alpha * z;
+    }
+  }
+}
+
+__global__ void lattice_from_global_kernel(const int* __restrict__ l2g, const unsigned char* __restrict__ owner,
+                                           long long n, int form, const double* __restrict__ g,
+                                           double* __restrict__ lat) {
+  const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+  if (i >= n) return;
+  const int d = l2g[i];
+  double v = 0.0;
+  if (d >= 0 && (form == 0 || owner[i])) v = g[d];
+  lat[i] = v;
+}
+
+__global__ void global_from_lattice_kernel(const int* __restrict__ rep_off, const int* __restrict__ rep_slot,
+                                           long long ndofs, int form, const double* __restrict__ lat,
+                                           double* __restrict__ g) {
+  const long long d = blockIdx.x * (long long)kThreads + threadIdx.x;
+  if (d >= ndofs) return;
+  if (form == 0) {
+    g[d] = lat[rep_slot[rep_off[d]]];
+  } else {
+    double s = 0.0;
+    for (int q = rep_off[d]; q < rep_off[d + 1]; ++q) s += lat[rep_slot[q]];
+    g[d] = s;
+  }
+}
+
+__global__ void coarse_gather_kernel(const int* __restrict__ rep_off, const int* __restrict__ rep_slot, int n0,
+                                     const double* __restrict__ r, double* __restrict__ rhs) {
+  const int d = blockIdx.x * kThreads + threadIdx.x;
+  if (d >= n0) return;
+  double s = 0.0;
+  for (int q = rep_off[d]; q < rep_off[d + 1]; ++q) s += r[rep_slot[q]];
+  rhs[d] = s;
+}
+
+// x = Ainv rhs, one warp per row, fixed lane-strided order + shuffle tree
+__global__ void coarse_gemv_kernel(const double* __restrict__ Ainv, int n0, const double* __restrict__ rhs,
+                                   double* __restrict__ x) {
+  const int warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n0) return;
+  const double* row = Ainv + (long long)warp * n0;
+  double s = 0.0;
+  for (int j = lane; j < n0; j += 32) s = fma(row[j], rhs[j], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) x[warp] = s;
+}
+
+__global__ void coarse_scatter_kernel(const int* __restrict__ l2g, long long n, const double* __restrict__ x,
+                                      double* __restrict__ out) {
+  const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+  if (i >= n) return;
+  const int d = l2g[i];
+  out[i] = d >= 0 ? x[d] : 0.0;
+}
+
+// One tensor axis of the two-scale kronecker product over K patches
+// (apply_along_axis(TwoScale), tensor.cpp:52-102); each thread one output.
+__global__ void ts_axis_kernel(TsDev ts, int transpose, int K, int d, int in0, int in1, int in2, int axis,
+                               const double* __restrict__ in, double* __restrict__ out) {
+  int dims_in[3] = {in0, in1, in2};
+  int dims_out[3] = {in0, in1, in2};
+  dims_out[axis] = transpose ? ts.coarse_dim : ts.fine_dim;
+  long long inner = 1, outer = 1;
+  for (int a = 0; a < axis; ++a) inner *= dims_in[a];
+  for (int a = axis + 1; a < d; ++a) outer *= dims_in[a];
+  const int m_in = dims_in[axis], m_out = dims_out[axis];
+  const long long per_in = inner * m_in * outer, per_out = inner * m_out * outer;
+  const long long total = per_out * K;
+  for (long long idx = blockIdx.x * (long long)kThreads + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * kThreads) {
+    const long long k = idx / per_out;
+    const long long rem = idx - k * per_out;
+    const long long t = rem % inner;
+    const int j = int((rem / inner) % m_out);
+    const long long o = rem / (inner * m_out);
+    const double* src = in + k * per_in + o * inner * m_in + t;
+    double s = 0.0;
+    if (!transpose) {
+      const double* v = ts.vals + ts.row_off[j];
+      const int st = ts.row_start[j];
+      for (int q = 0; q < ts.row_len[j]; ++q) s = fma(v[q], src[(long long)(st + q) * inner], s);
+    } else {
+      for (int q = ts.col_off[j]; q < ts.col_off[j + 1]; ++q) s = fma(ts.col_val[q], src[(long long)ts.col_row[q] * inner], s);
+    }
+    out[idx] = s;
+  }
+}
+
+__global__ void masked_axpy_kernel(const int* __restrict__ l2g, long long n, double c, const double* __restrict__ val,
+                                   double* __restrict__ u) {
+  const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+  if (i >= n) return;
+  if (l2g[i] >= 0) u[i] += c * val[i];
+}
+
+__global__ void mask_dirichlet_kernel(const int* __restrict__ l2g, long long n, double* __restrict__ v) {
+  const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
+  if (i >= n) return;
+  if (l2g[i] < 0) v[i] = 0.0;
+}
+
+__global__ void zero_dirichlet_band_kernel(int dim, int degree, int ext, long long S, int K, const int* __restrict__ l2g,
+                                           double* __restrict__ band) {
+  const int W = 2 * degree + 1;
+  const int O = dim == 2 ? W * W : W * W * W;
+  const long long total = (long long)K * O * S;
+  for (long long idx = blockIdx.x * (long long)kThreads + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * kThreads) {
+    const long long k = idx / (O * S);
+    const long long rem = idx - k * O * S;
+    const int o = int(rem / S);
+    const long long r = rem - (long long)o * S;
+    const int i0 = int(r % ext), i1 = int((r / ext) % ext), i2 = dim == 3 ? int(r / ((long long)ext * ext)) : 0;
+    const int d0 = o % W - degree, d1 = (o / W) % W - degree, d2 = dim == 3 ? o / (W * W) - degree : 0;
+    const int j0 = i0 + d0, j1 = i1 + d1, j2 = i2 + d2;
+    bool live = j0 >= 0 && j0 < ext && j1 >= 0 && j1 < ext && (dim == 2 || (j2 >= 0 && j2 < ext));
+    if (live) {
+      const long long c = j0 + (long long)ext * j1 + (long long)ext * ext * j2;
+      live = l2g[k * S + r] >= 0 && l2g[k * S + c] >= 0;
+    }
+    if (!live) band[idx] = 0.0;
+  }
+}
+
+// PCG scalars kept on device: [0] rz [1] pAp [2] alpha [3] rz_next [4] beta [5] |r|^2 [6] |r| [7] flag
+__global__ void pcg_scalars_kernel(int op, double* s) {
+  if (threadIdx.x != 0) return;
+  switch (op) {
+    case 0:  // alpha = rz / pAp; flag non-positive energy
+      if (!(s[1] > 0.0)) s[7] = 1.0;
+      s[2] = s[0] / s[1];
+      break;
+    case 1:  // beta = rz_next / rz; rz = rz_next
+      s[4] = s[3] / s[0];
+      s[0] = s[3];
+      break;
+    case 2:  // |r| = sqrt(|r|^2)
+      s[6] = sqrt(s[5]);
+      break;
+  }
+}
+
+}  // namespace
+
+void launch_fill(cudaStream_t s, double* x, long long n, double v) {
+  if (n > 0) fill_kernel<<<grid_for(n, 4), kThreads, 0, s>>>(x, n, v);
+}
+void launch_copy(cudaStream_t s, const double* x, double* y, long long n) {
+  if (n > 0) copy_kernel<<<grid_for(n, 4), kThreads, 0, s>>>(x, y, n);
+}
+void launch_axpy(cudaStream_t s, double a, const double* a_dev, double sign, const double* x, double* y, long long n) {
+  if (n > 0) axpy_kernel<<<grid_for(n, 4), kThreads, 0, s>>>(a, a_dev, sign, x, y, n);
+}
+void launch_xpay(cudaStream_t s, const double* z, double beta, const double* beta_dev, double* p, long long n) {
+  if (n > 0) xpay_kernel<<<grid_for(n, 4), kThreads, 0, s>>>(z, beta, beta_dev, p, n);
+}
+void launch_scale_set(cudaStream_t s, double a, const double* x, double* y, long long n) {
+  if (n > 0) scale_set_kernel<<<grid_for(n, 4), kThreads, 0, s>>>(a, x, y, n);
+}
+int dot_blocks(long long n) {
+  long long g = (n + kThreads * 8 - 1) / (kThreads * 8);
+  if (g > 1184) g = 1184;
+  return int(g < 1 ? 1 : g);
+}
+void launch_dot_partial(cudaStream_t s, const double* a, const double* b, long long n, double* partial) {
+  dot_partial_kernel<<<dot_blocks(n), kThreads, 0, s>>>(a, b, n, partial);
+}
+void launch_sum_partials(cudaStream_t s, const double* partial, int nparts, double* out) {
+  sum_partials_kernel<<<1, kThreads, 0, s>>>(partial, nparts, out);
+}
+void launch_group_sum(cudaStream_t s, const int* goff, const int* gslot, int ngroups, const double* r, double* out) {
+  if (ngroups > 0) group_sum_kernel<<<grid_for(ngroups), kThreads, 0, s>>>(goff, gslot, ngroups, r, out);
+}
+void launch_gather_sum(cudaStream_t s, const int* dof_g, long long ndof, const int* rep_off, const int* rep_slot,
+                       const double* r, double* buf) {
+  if (ndof > 0) gather_sum_kernel<<<grid_for(ndof), kThreads, 0, s>>>(dof_g, ndof, rep_off, rep_slot, r, buf);
+}
+void launch_scatter(cudaStream_t s, const int* dof_g, long long ndof, const int* rep_off, const int* rep_slot,
+                    const double* buf, double* out, int add, double alpha) {
+  if (ndof > 0)
+    scatter_kernel<<<grid_for(ndof), kThreads, 0, s>>>(dof_g, ndof, rep_off, rep_slot, buf, out, add, alpha);
+}
+void launch_edges_vertices(cudaStream_t s, const EdgePiece* edges, int nedges, const int* edge_dof_g,
+                           const int* vert_g, const double* vert_scalar, int nverts, const int* rep_off,
+                           const int* rep_slot, const double* r, double* out, int add, double alpha) {
+  const int grid = nedges + (nverts > 0 ? 1 : 0);
+  if (grid > 0)
+    edges_vertices_kernel<<<grid, kThreads, 0, s>>>(edges, nedges, edge_dof_g, vert_g, vert_scalar, nverts, rep_off,
+                                                    rep_slot, r, out, add, alpha);
+}
+void launch_lattice_from_global(cudaStream_t s, const int* l2g, const unsigned char* owner, long long n, int form,
+                                const double* g, double* lat) {
+  if (n > 0) lattice_from_global_kernel<<<grid_for(n), kThreads, 0, s>>>(l2g, owner, n, form, g, lat);
+}
+void launch_global_from_lattice(cudaStream_t s, const int* rep_off, const int* rep_slot, long long ndofs, int form,
+                                const double* lat, double* g) {
+  if (ndofs > 0) global_from_lattice_kernel<<<grid_for(ndofs), kThreads, 0, s>>>(rep_off, rep_slot, ndofs, form, lat, g);
+}
+void launch_coarse(cudaStream_t s, const int* rep_off, const int* rep_slot, const int* l2g, int n0, long long lat_n,
+                   const double* Ainv, const double* r, double* rhs, double* x, double* out) {
+  if (n0 > 0) {
+    coarse_gather_kernel<<<grid_for(n0), kThreads, 0, s>>>(rep_off, rep_slot, n0, r, rhs);
+    coarse_gemv_kernel<<<grid_for((long long)n0 * 32), kThreads, 0, s>>>(Ainv, n0, rhs, x);
+  }
+  coarse_scatter_kernel<<<grid_for(lat_n), kThreads, 0, s>>>(l2g, lat_n, x, out);
+}
+void launch_ts_axis(cudaStream_t s, const TsDev& ts, bool transpose, int K, int d, const int* in_dims, int axis,
+                    const double* in, double* out) {
+  long long per_out = 1;
+  for (int a = 0; a < d; ++a) per_out *= (a == axis ? (transpose ? ts.coarse_dim : ts.fine_dim) : in_dims[a]);
+  const long long total = per_out * K;
+  long long g = (total + kThreads - 1) / kThreads;
+  if (g > 148LL * 32) g = 148LL * 32;
+  ts_axis_kernel<<<int(g < 1 ? 1 : g), kThreads, 0, s>>>(ts, transpose ? 1 : 0, K, d, in_dims[0], in_dims[1],
+                                                         d == 3 ? in_dims[2] : 1, axis, in, out);
+}
+void launch_masked_axpy(cudaStream_t s, const int* l2g, long long n, double c, const double* val, double* u) {
+  if (n > 0) masked_axpy_kernel<<<grid_for(n), kThreads, 0, s>>>(l2g, n, c, val, u);
+}
+void launch_mask_dirichlet(cudaStream_t s, const int* l2g, long long n, double* v) {
+  if (n > 0) mask_dirichlet_kernel<<<grid_for(n), kThreads, 0, s>>>(l2g, n, v);
+}
+void launch_zero_dirichlet_band(cudaStream_t s, int dim, int degree, int ext, long long S, int K, const int* l2g,
+                                double* band) {
+  zero_dirichlet_band_kernel<<<148 * 32, kThreads, 0, s>>>(dim, degree, ext, S, K, l2g, band);
+}
+void launch_pcg_scalars(cudaStream_t s, int op, double* scal) { pcg_scalars_kernel<<<1, 32, 0, s>>>(op, scal); }
+
+}  // namespace pmgcu
