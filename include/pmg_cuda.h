@@ -114,6 +114,16 @@ int pmg_pcg_solve(pmg_ctx* ctx, const double* f_host, int64_t n, double tol, int
  * which = 1 launches of the band SpMV; which = 2 reset counters. */
 int pmg_kernel_stats(pmg_ctx* ctx, int which, int64_t* count, double* reserved);
 
+/* Live kernel timing with CUDA events on the launch stream.  While enabled,
+ * every launch of the timed classes is bracketed by two events.
+ * kernel_class: 0 = band SpMV, 1 = fast-diagonalization pass.
+ * pmg_profile_read synchronizes and returns, for launches on `level` since the
+ * last read: the launch count, the summed device milliseconds and the summed
+ * algorithmic bytes (SpMV: 8 B per stored reference entry + 8 B per lattice
+ * row for x, y and f when read) or flops (FD: 2 per multiply-add). */
+int pmg_profile(pmg_ctx* ctx, int enable);
+int pmg_profile_read(pmg_ctx* ctx, int kernel_class, int level, int64_t* launches, double* ms, double* work);
+
 #ifdef __cplusplus
 }
 #endif

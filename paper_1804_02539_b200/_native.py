@@ -111,7 +111,7 @@ CUDA_SYMBOLS = [
     "pmg_apply_op", "pmg_residual", "pmg_accumulate", "pmg_smooth", "pmg_restrict", "pmg_add_prolonged",
     "pmg_coarse_solve", "pmg_dot", "pmg_axpy", "pmg_xpay",
     "pmg_mg_cycle", "pmg_precondition", "pmg_pcg_solve_device", "pmg_pcg_solve",
-    "pmg_kernel_stats", "pmg_synchronize",
+    "pmg_kernel_stats", "pmg_synchronize", "pmg_profile", "pmg_profile_read",
 ]
 
 
@@ -156,5 +156,7 @@ def cuda_lib():
                                              C.POINTER(C.c_int)])
         _sig(lib, "pmg_kernel_stats", C.c_int, [_vp, C.c_int, C.POINTER(C.c_int64), _dp])
         _sig(lib, "pmg_synchronize", C.c_int, [_vp])
+        _sig(lib, "pmg_profile", C.c_int, [_vp, C.c_int])
+        _sig(lib, "pmg_profile_read", C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_int64), _dp, _dp])
         _cuda = lib
     return _cuda

@@ -219,8 +219,9 @@ class GpuBackend:
         self._check(rc)
         return u, SolveReport(it.value, list(hist[: it.value + 1]))
 
-    def pcg_solve_device(self, f: DistVec, tol: float = 1e-8, max_iter: int = 500):
-        u = AccVec(self, f.level)
+    def pcg_solve_device(self, f: DistVec, tol: float = 1e-8, max_iter: int = 500, u: AccVec | None = None):
+        if u is None:
+            u = AccVec(self, f.level)
         hist = np.zeros(max_iter + 1)
         it = C.c_int(0)
         self._check(self._lib.pmg_pcg_solve_device(self._ctx, f._h, tol, max_iter, u._h,

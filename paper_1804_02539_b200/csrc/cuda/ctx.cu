@@ -15,6 +15,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -53,20 +54,21 @@ struct DevLevel {
   // interior FD
   FdPiece* d_int = nullptr;
   int n_int = 0;
-  bool int_wide = false;
-  int2* int_items[6] = {};
+  int4* int_items[6] = {};
   int n_int_items[6] = {};
+  std::vector<std::array<int, 3>> int_dims;  // host copy for flop counts
   // faces
   FdPiece* d_face = nullptr;
   int n_face = 0;
-  bool face_wide = false;
   int* face_dof_g = nullptr;
   long long face_ndof = 0;
-  int2* face_items[4] = {};
+  int4* face_items[4] = {};
   int n_face_items[4] = {};
   // edges / vertices
   EdgePiece* d_edges = nullptr;
   int n_edges = 0;
+  int2* edge_items = nullptr;
+  int n_edge_items = 0;
   int* edge_dof_g = nullptr;
   int* vert_g = nullptr;
   double* vert_scalar = nullptr;
@@ -108,6 +110,25 @@ struct pmg_ctx {
   size_t bytes = 0;
   long long launches = 0, spmv_launches = 0;
   std::string err;
+  // live event timing (pmg_profile)
+  bool profiling = false;
+  struct Timed {
+    int cls, level;
+    double work;
+    cudaEvent_t a, b;
+  };
+  std::vector<Timed> timed;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t get_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+  }
 
   template <class T>
   T* alloc(size_t count) {
@@ -130,6 +151,11 @@ struct pmg_ctx {
   }
   ~pmg_ctx() {
     cudaSetDevice(device);
+    for (auto& t : timed) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+    for (auto e : event_pool) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
     if (h_scal) cudaFreeHost(h_scal);
     if (own_stream) cudaStreamDestroy(own_stream);
@@ -148,7 +174,8 @@ namespace {
 thread_local std::string g_create_error;
 
 // Explicit inverse of the banded Cholesky operator: column j is the
-// reference BandedCholesky::solve (banded.cpp:61-77) of e_j; stored row-major.
+// reference BandedCholesky::solve (banded.cpp:61-77) of e_j; stored
+// column-major so a warp's rows read consecutive addresses.
 std::vector<double> banded_inverse(int n, int bw, const double* l) {
   const int w = bw + 1;
   std::vector<double> inv(size_t(n) * n), y(n);
@@ -163,7 +190,7 @@ std::vector<double> banded_inverse(int n, int bw, const double* l) {
       for (int k = i + 1; k < std::min(n, i + bw + 1); ++k) s -= l[size_t(k) * w + (k - i)] * y[k];
       y[i] = s / l[size_t(i) * w];
     }
-    for (int i = 0; i < n; ++i) inv[size_t(i) * n + j] = y[i];
+    for (int i = 0; i < n; ++i) inv[size_t(j) * n + i] = y[i];
   }
   return inv;
 }
@@ -364,6 +391,7 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
       }
       fp.diag = diag_of(pc.diag, fp.total);
       h_int.push_back(fp);
+      L.int_dims.push_back({fp.dims[0], fp.dims[1], fp.dims[2]});
     } else if (pc.kind == PMG_PIECE_FACE) {
       FdPiece fp{};
       fp.naxes = 2;
@@ -404,10 +432,8 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
       vert_scalar.push_back(pc.scalar);
     }
   }
-  if (maxdim_int > 288 || maxdim_face > 288)
-    throw PmgError(PMG_ERR_CONFIG, "fast-diagonalization pieces wider than 288 dofs per axis are not supported");
-  L.int_wide = maxdim_int > 72;
-  L.face_wide = maxdim_face > 72;
+  (void)maxdim_int;
+  (void)maxdim_face;
   L.n_int = int(h_int.size());
   L.d_int = c.upload(h_int);
   L.n_face = int(h_face.size());
@@ -416,24 +442,34 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   L.face_ndof = (long long)face_dofs.size();
   L.n_edges = int(h_edges.size());
   L.d_edges = c.upload(h_edges);
+  {
+    std::vector<int2> ei;
+    for (int e = 0; e < L.n_edges; ++e)
+      for (int r0 = 0; r0 < h_edges[e].m; r0 += 32) ei.push_back(make_int2(e, r0));
+    L.n_edge_items = int(ei.size());
+    L.edge_items = c.upload(ei);
+  }
   L.edge_dof_g = c.upload(edge_dofs);
   L.n_verts = int(vert_g.size());
   L.vert_g = c.upload(vert_g);
   L.vert_scalar = c.upload(vert_scalar);
-  auto make_items = [&](const std::vector<FdPiece>& ps, int naxes, bool wide, int2** items, int* counts) {
-    const int BM = fd_rows_per_block(wide);
+  // CTA work items of every pass: (piece, row panel, column panel)
+  auto make_items = [&](const std::vector<FdPiece>& ps, int naxes, int4** items, int* counts) {
+    const int BM = fd_rows_per_block(), BN = fd_cols_per_block();
     for (int pass = 0; pass < 2 * naxes; ++pass) {
-      std::vector<int2> it;
+      std::vector<int4> it;
       for (int i = 0; i < int(ps.size()); ++i) {
-        const long long R = ps[i].total / ps[i].dims[pass % naxes];
-        for (long long r0 = 0; r0 < R; r0 += BM) it.push_back(make_int2(i, int(r0)));
+        const int K = ps[i].dims[pass % naxes];
+        const long long R = ps[i].total / K;
+        for (long long r0 = 0; r0 < R; r0 += BM)
+          for (int n0 = 0; n0 < K; n0 += BN) it.push_back(make_int4(i, int(r0), n0, 0));
       }
       counts[pass] = int(it.size());
       items[pass] = c.upload(it);
     }
   };
-  make_items(h_int, d, L.int_wide, L.int_items, L.n_int_items);
-  if (d == 3) make_items(h_face, 2, L.face_wide, L.face_items, L.n_face_items);
+  make_items(h_int, d, L.int_items, L.n_int_items);
+  if (d == 3) make_items(h_face, 2, L.face_items, L.n_face_items);
 
   // ---- two-scale factor (TransferOperator ctor, transfer.cpp:10-19)
   if (l >= 1) {
@@ -535,12 +571,52 @@ void build_ctx(pmg_ctx& c, const pmg_hierarchy_desc& D) {
 // ================================================================ operations
 // All launch on c.stream and count their kernels.
 
+struct TimedScope {
+  pmg_ctx& c;
+  pmg_ctx::Timed t{};
+  bool on;
+  TimedScope(pmg_ctx& ctx, int cls, int level, double work) : c(ctx), on(ctx.profiling) {
+    if (!on) return;
+    t = pmg_ctx::Timed{cls, level, work, c.get_event(), c.get_event()};
+    ck(cudaEventRecord(t.a, c.stream), "cudaEventRecord");
+  }
+  ~TimedScope() {
+    if (!on) return;
+    cudaEventRecord(t.b, c.stream);
+    c.timed.push_back(t);
+  }
+};
+
+// reference CSR entries per level (harness.cpp:274-282) for one patch
+long long stored_per_patch(int degree, int elements, int dim) {
+  const int extent = elements + degree;
+  long long pairs = 0;
+  for (int i = 0; i < extent; ++i) pairs += std::min(i + degree, extent - 1) - std::max(i - degree, 0) + 1;
+  long long pp = 1;
+  for (int a = 0; a < dim; ++a) pp *= pairs;
+  return pp;
+}
+
 void op_spmv(pmg_ctx& c, int l, const double* x, const double* f, double* y, double* dot_partial = nullptr) {
   const DevLevel& L = c.lv[l];
+  const double bytes = 8.0 * double(stored_per_patch(c.degree, L.n, c.dim)) * L.K + 8.0 * L.lat_n * (f ? 3 : 2);
+  TimedScope ts(c, 0, l, bytes);
   SpmvArgs a{c.dim, c.degree, L.ext, L.S, L.K, L.band, x, f, y, dot_partial};
   launch_spmv(c.stream, a);
   c.launches++;
   c.spmv_launches++;
+}
+
+// flops of one pass over every interior piece of a level: 2 R K N per piece
+double fd_pass_flops(const DevLevel& L, const std::vector<std::array<int, 3>>& dims, int naxes, int pass) {
+  (void)L;
+  double f = 0.0;
+  for (const auto& d : dims) {
+    double tot = 1.0;
+    for (int a = 0; a < naxes; ++a) tot *= d[a];
+    f += 2.0 * tot * d[pass % naxes];
+  }
+  return f;
 }
 
 // smooth: interior FD, faces, edges + vertices.  out_mode SET: out = alpha z
@@ -554,8 +630,9 @@ void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double
     int out_mode = FD_OUT_WORK;
     if (pass == d - 1) out_mode = FD_OUT_WORK_DIAG;
     if (pass == np - 1) out_mode = add ? FD_OUT_LATTICE_ADD : FD_OUT_LATTICE_SET;
-    launch_fd_pass(c.stream, L.int_wide, L.d_int, L.int_items[pass], L.n_int_items[pass], pass, d, in_mode, out_mode,
-                   r, out, alpha, c.work[(pass + 1) & 1], c.work[pass & 1]);
+    TimedScope ts(c, 1, l, fd_pass_flops(L, L.int_dims, d, pass));
+    launch_fd_pass(c.stream, L.d_int, L.int_items[pass], L.n_int_items[pass], pass, d, in_mode, out_mode, r, out,
+                   alpha, c.work[(pass + 1) & 1], c.work[pass & 1]);
     if (L.n_int_items[pass]) c.launches++;
   }
   if (d == 3 && L.n_face > 0) {
@@ -563,16 +640,16 @@ void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double
     c.launches++;
     for (int pass = 0; pass < 4; ++pass) {
       const int out_mode = pass == 1 ? FD_OUT_WORK_DIAG : FD_OUT_WORK;
-      launch_fd_pass(c.stream, L.face_wide, L.d_face, L.face_items[pass], L.n_face_items[pass], pass, 2, FD_IN_WORK,
-                     out_mode, nullptr, nullptr, 0.0, c.face_buf[(pass + 1) & 1], c.face_buf[pass & 1]);
+      launch_fd_pass(c.stream, L.d_face, L.face_items[pass], L.n_face_items[pass], pass, 2, FD_IN_WORK, out_mode,
+                     nullptr, nullptr, 0.0, c.face_buf[(pass + 1) & 1], c.face_buf[pass & 1]);
       c.launches++;
     }
     launch_scatter(c.stream, L.face_dof_g, L.face_ndof, L.rep_off, L.rep_slot, c.face_buf[1], out, add ? 1 : 0, alpha);
     c.launches++;
   }
   if (L.n_edges + L.n_verts > 0) {
-    launch_edges_vertices(c.stream, L.d_edges, L.n_edges, L.edge_dof_g, L.vert_g, L.vert_scalar, L.n_verts, L.rep_off,
-                          L.rep_slot, r, out, add ? 1 : 0, alpha);
+    launch_edges_vertices(c.stream, L.d_edges, L.edge_items, L.n_edge_items, L.edge_dof_g, L.vert_g, L.vert_scalar,
+                          L.n_verts, L.rep_off, L.rep_slot, r, out, add ? 1 : 0, alpha);
     c.launches++;
   }
 }
@@ -1058,6 +1135,36 @@ int pmg_pcg_solve(pmg_ctx* ctx, const double* f_host, int64_t n, double tol, int
   if (g != PMG_OK) return g;
   if (rc == PMG_ERR_DIVERGENCE) ctx->err = "pcg: no convergence within the iteration limit";
   return rc;
+}
+
+int pmg_profile(pmg_ctx* ctx, int enable) {
+  return guarded(ctx, [&] { ctx->profiling = enable != 0; });
+}
+
+int pmg_profile_read(pmg_ctx* ctx, int kernel_class, int level, int64_t* launches, double* ms, double* work) {
+  return guarded(ctx, [&] {
+    sync_check(*ctx);
+    int64_t n = 0;
+    double t = 0.0, w = 0.0;
+    std::vector<pmg_ctx::Timed> keep;
+    for (auto& e : ctx->timed) {
+      if (e.cls == kernel_class && e.level == level) {
+        float dt = 0.f;
+        ck(cudaEventElapsedTime(&dt, e.a, e.b), "cudaEventElapsedTime");
+        n++;
+        t += dt;
+        w += e.work;
+        ctx->event_pool.push_back(e.a);
+        ctx->event_pool.push_back(e.b);
+      } else {
+        keep.push_back(e);
+      }
+    }
+    ctx->timed.swap(keep);
+    *launches = n;
+    *ms = t;
+    *work = w;
+  });
 }
 
 int pmg_kernel_stats(pmg_ctx* ctx, int which, int64_t* count, double* reserved) {

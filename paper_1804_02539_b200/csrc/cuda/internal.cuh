@@ -37,11 +37,12 @@ enum FdIn { FD_IN_WORK = 0, FD_IN_LATTICE = 1 };
 enum FdOut { FD_OUT_WORK = 0, FD_OUT_WORK_DIAG = 1, FD_OUT_LATTICE_SET = 2, FD_OUT_LATTICE_ADD = 3 };
 
 // One fast-diagonalization pass (contract one axis, rotate the layout).
-// items: (piece, first row) per CTA; wide = true selects the N <= 288 tile.
-void launch_fd_pass(cudaStream_t s, bool wide, const FdPiece* pieces, const int2* items, int nitems, int pass,
-                    int naxes, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
+// items: (piece, first row, first column, 0) per CTA.
+void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int pass, int naxes,
+                    int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
                     const double* work_in, double* work_out);
-int fd_rows_per_block(bool wide);
+int fd_rows_per_block();
+int fd_cols_per_block();
 void fd_configure();  // per device, before the first pass
 
 // ---------------------------------------------------------------- SpMV
@@ -79,11 +80,13 @@ void launch_scatter(cudaStream_t s, const int* dof_g, long long ndof, const int*
 struct EdgePiece {
   int m;
   long long dof_off;  // into the concatenated edge dof list
-  const double* Linv; // row-major m x m
+  const double* Linv; // column-major m x m
 };
-void launch_edges_vertices(cudaStream_t s, const EdgePiece* edges, int nedges, const int* edge_dof_g,
-                           const int* vert_g, const double* vert_scalar, int nverts, const int* rep_off,
-                           const int* rep_slot, const double* r, double* out, int add, double alpha);
+// items: (edge, first row) per CTA, 32 rows each
+void launch_edges_vertices(cudaStream_t s, const EdgePiece* edges, const int2* items, int nitems,
+                           const int* edge_dof_g, const int* vert_g, const double* vert_scalar, int nverts,
+                           const int* rep_off, const int* rep_slot, const double* r, double* out, int add,
+                           double alpha);
 // global <-> lattice
 void launch_lattice_from_global(cudaStream_t s, const int* l2g, const unsigned char* owner, long long n, int form,
                                 const double* g, double* lat);

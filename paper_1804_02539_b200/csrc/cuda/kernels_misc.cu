@@ -112,16 +112,20 @@ __global__ void scatter_kernel(const int* __restrict__ dof_g, long long ndof, co
 }
 
 // Edge pieces: z = L_T^-1 (sum of replica shares) with the explicit inverse of
-// the banded operator (BandedCholesky::solve, banded.cpp:61-77), one CTA per
-// edge; the trailing CTA handles every vertex piece (smoother.cpp:36-38).
+// the banded operator (BandedCholesky::solve, banded.cpp:61-77).  One CTA per
+// (edge, 32-row chunk): lane = row, the 8 warps split the columns, partial
+// sums meet in shared memory in a fixed order.  The trailing CTA handles every
+// vertex piece (smoother.cpp:36-38).
 __global__ void __launch_bounds__(kThreads) edges_vertices_kernel(
-    const EdgePiece* __restrict__ edges, int nedges, const int* __restrict__ edge_dof_g,
-    const int* __restrict__ vert_g, const double* __restrict__ vert_scalar, int nverts,
-    const int* __restrict__ rep_off, const int* __restrict__ rep_slot, const double* __restrict__ r,
+    const EdgePiece* __restrict__ edges, const int2* __restrict__ items, int nitems,
+    const int* __restrict__ edge_dof_g, const int* __restrict__ vert_g, const double* __restrict__ vert_scalar,
+    int nverts, const int* __restrict__ rep_off, const int* __restrict__ rep_slot, const double* __restrict__ r,
     double* __restrict__ out, int add, double alpha) {
   __shared__ double buf[512];
-  if (blockIdx.x < nedges) {
-    const EdgePiece e = edges[blockIdx.x];
+  __shared__ double part[kThreads / 32][32];
+  if (blockIdx.x < nitems) {
+    const int2 it = items[blockIdx.x];
+    const EdgePiece e = edges[it.x];
     const int* dofs = edge_dof_g + e.dof_off;
     for (int i = threadIdx.x; i < e.m; i += kThreads) {
       const int g = dofs[i];
@@ -130,10 +134,24 @@ __global__ void __launch_bounds__(kThreads) edges_vertices_kernel(
       buf[i] = s;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < e.m; i += kThreads) {
-      const double* row = e.Linv + (long long)i * e.m;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = it.y + lane;
+    const int per = (e.m + 7) / 8;
+    const int j0 = warp * per, j1 = min(e.m, j0 + per);
+    double z0 = 0.0, z1 = 0.0;
+    if (i < e.m) {
+      int j = j0;
+      for (; j + 1 < j1; j += 2) {
+        z0 = fma(e.Linv[(long long)j * e.m + i], buf[j], z0);
+        z1 = fma(e.Linv[(long long)(j + 1) * e.m + i], buf[j + 1], z1);
+      }
+      if (j < j1) z0 = fma(e.Linv[(long long)j * e.m + i], buf[j], z0);
+    }
+    part[warp][lane] = z0 + z1;
+    __syncthreads();
+    if (warp == 0 && i < e.m) {
       double z = 0.0;
-      for (int j = 0; j < e.m; ++j) z = fma(row[j], buf[j], z);
+      for (int w = 0; w < kThreads / 32; ++w) z += part[w][lane];
       const int g = dofs[i];
       for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) {
         if (add)
@@ -340,13 +358,14 @@ void launch_scatter(cudaStream_t s, const int* dof_g, long long ndof, const int*
   if (ndof > 0)
     scatter_kernel<<<grid_for(ndof), kThreads, 0, s>>>(dof_g, ndof, rep_off, rep_slot, buf, out, add, alpha);
 }
-void launch_edges_vertices(cudaStream_t s, const EdgePiece* edges, int nedges, const int* edge_dof_g,
-                           const int* vert_g, const double* vert_scalar, int nverts, const int* rep_off,
-                           const int* rep_slot, const double* r, double* out, int add, double alpha) {
-  const int grid = nedges + (nverts > 0 ? 1 : 0);
+void launch_edges_vertices(cudaStream_t s, const EdgePiece* edges, const int2* items, int nitems,
+                           const int* edge_dof_g, const int* vert_g, const double* vert_scalar, int nverts,
+                           const int* rep_off, const int* rep_slot, const double* r, double* out, int add,
+                           double alpha) {
+  const int grid = nitems + (nverts > 0 ? 1 : 0);
   if (grid > 0)
-    edges_vertices_kernel<<<grid, kThreads, 0, s>>>(edges, nedges, edge_dof_g, vert_g, vert_scalar, nverts, rep_off,
-                                                    rep_slot, r, out, add, alpha);
+    edges_vertices_kernel<<<grid, kThreads, 0, s>>>(edges, items, nitems, edge_dof_g, vert_g, vert_scalar, nverts,
+                                                    rep_off, rep_slot, r, out, add, alpha);
 }
 void launch_lattice_from_global(cudaStream_t s, const int* l2g, const unsigned char* owner, long long n, int form,
                                 const double* g, double* lat) {

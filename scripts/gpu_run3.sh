@@ -1,0 +1,3 @@
+python scripts/solve_once.py c2 1 > gpurun_out/solve_once.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python scripts/solve_once.py c2 1 > gpurun_out/ncu_c2.log 2>&1
+echo "ncu rc=$?"; tail -2 gpurun_out/ncu_c2.log; wc -l gpurun_out/launches_c2.csv
