@@ -42,7 +42,7 @@ void ck(cudaError_t e, const char* what) {
 
 struct DevLevel {
   int n = 0, ext = 0, O = 0, K = 0;
-  long long S = 0, lat_n = 0, N = 0;
+  long long S = 0, Sp = 0, lat_n = 0, N = 0;
   double* band = nullptr;
   int* l2g = nullptr;
   unsigned char* owner = nullptr;
@@ -119,6 +119,44 @@ struct pmg_ctx {
   };
   std::vector<Timed> timed;
   std::vector<cudaEvent_t> event_pool;
+  // CUDA graphs of the PCG iteration (captured on own_stream, launched on stream)
+  bool use_graphs = true;
+  cudaGraphExec_t graph_front = nullptr, graph_back = nullptr;
+  long long graph_front_launches = 0, graph_back_launches = 0;
+  const double* graph_u = nullptr;
+  cudaEvent_t ev_norm = nullptr;
+
+  template <class F>
+  void capture(cudaGraphExec_t& exec, long long& nlaunch, F&& body) {
+    if (exec) {
+      cudaGraphExecDestroy(exec);
+      exec = nullptr;
+    }
+    cudaStream_t saved = stream;
+    stream = own_stream;
+    const long long before = launches;
+    ck(cudaStreamBeginCapture(own_stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    cudaGraph_t g = nullptr;
+    try {
+      body();
+    } catch (...) {
+      cudaStreamEndCapture(own_stream, &g);
+      if (g) cudaGraphDestroy(g);
+      stream = saved;
+      launches = before;
+      throw;
+    }
+    stream = saved;
+    ck(cudaStreamEndCapture(own_stream, &g), "cudaStreamEndCapture");
+    ck(cudaGraphInstantiate(&exec, g, 0), "cudaGraphInstantiate");
+    cudaGraphDestroy(g);
+    nlaunch = launches - before;
+    launches = before;
+  }
+  void launch_graph(cudaGraphExec_t exec, long long n) {
+    ck(cudaGraphLaunch(exec, stream), "cudaGraphLaunch");
+    launches += n;
+  }
   cudaEvent_t get_event() {
     if (!event_pool.empty()) {
       cudaEvent_t e = event_pool.back();
@@ -151,6 +189,9 @@ struct pmg_ctx {
   }
   ~pmg_ctx() {
     cudaSetDevice(device);
+    if (graph_front) cudaGraphExecDestroy(graph_front);
+    if (graph_back) cudaGraphExecDestroy(graph_back);
+    if (ev_norm) cudaEventDestroy(ev_norm);
     for (auto& t : timed) {
       cudaEventDestroy(t.a);
       cudaEventDestroy(t.b);
@@ -235,11 +276,13 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   const int* l2g_all = ld.l2g;
   const int* l2g = l2g_all + (size_t)c.pb * S;
 
-  // ---- band
-  L.band = c.alloc<double>(size_t(L.K) * L.O * S);
+  // ---- band: rows of one (patch, offset) pair at stride Sp (>= S, see spmv_padded_rows)
+  L.Sp = spmv_padded_rows(d, p, S);
+  const long long Sp = L.Sp;
+  L.band = c.alloc<double>(size_t(L.K) * L.O * Sp);
   if (ld.band_format == PMG_BAND_TENSOR) {
-    ck(cudaMemcpy(L.band, ld.band + (size_t)c.pb * L.O * S, sizeof(double) * size_t(L.K) * L.O * S,
-                  cudaMemcpyHostToDevice),
+    ck(cudaMemcpy2D(L.band, sizeof(double) * Sp, ld.band + (size_t)c.pb * L.O * S, sizeof(double) * S,
+                    sizeof(double) * S, size_t(L.K) * L.O, cudaMemcpyHostToDevice),
        "band upload");
   } else if (ld.band_format == PMG_BAND_CSR) {
     // place every CSR entry at its tensor offset (PatchOperator, assembly.hpp:16-25)
@@ -264,14 +307,15 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
           }
           hb[size_t(o) * S + r] += vals[q];
         }
-      ck(cudaMemcpy(L.band + size_t(k) * L.O * S, hb.data(), sizeof(double) * hb.size(), cudaMemcpyHostToDevice),
+      ck(cudaMemcpy2D(L.band + size_t(k) * L.O * Sp, sizeof(double) * Sp, hb.data(), sizeof(double) * S,
+                      sizeof(double) * S, size_t(L.O), cudaMemcpyHostToDevice),
          "band upload");
     }
   } else {
     throw PmgError(PMG_ERR_CONFIG, "unknown band format");
   }
   L.l2g = c.upload(l2g, size_t(L.lat_n));
-  launch_zero_dirichlet_band(c.stream, d, p, L.ext, S, L.K, L.l2g, L.band);
+  launch_zero_dirichlet_band(c.stream, d, p, L.ext, S, Sp, L.K, L.l2g, L.band);
 
   // ---- replicas: global owner patch over all patches; local replica CSR
   std::vector<int> owner_patch(size_t(L.N), -1);
@@ -552,7 +596,8 @@ void build_ctx(pmg_ctx& c, const pmg_hierarchy_desc& D) {
   c.coarse_x = c.alloc<double>(size_t(c.n0));
   long long maxlat = 0;
   for (auto& L : c.lv) maxlat = std::max(maxlat, L.lat_n);
-  c.partial_n = std::max(spmv_blocks(maxlat), dot_blocks(maxlat));
+  c.partial_n = dot_blocks(maxlat);
+  for (auto& L : c.lv) c.partial_n = std::max(c.partial_n, spmv_partials(c.dim, c.degree, L.S, L.K));
   c.partial = c.alloc<double>(size_t(c.partial_n));
   c.scal = c.alloc<double>(16);
   ck(cudaMemset(c.scal, 0, 16 * sizeof(double)), "memset");
@@ -661,14 +706,13 @@ void op_restrict(pmg_ctx& c, int l, const double* r, double* out) {
   int dims[3] = {F.ext, F.ext, F.ext};
   const double* src = r;
   for (int a = 0; a < c.dim; ++a) {
-    double* dst = (a == c.dim - 1) ? out : c.tbuf[a & 1];
-    launch_ts_axis(c.stream, F.ts, true, F.K, c.dim, dims, a, src, dst);
+    const bool last = a == c.dim - 1;
+    double* dst = last ? out : c.tbuf[a & 1];
+    launch_ts_axis(c.stream, F.ts, true, F.K, c.dim, dims, a, src, dst, last ? 1 : 0, C.l2g);
     c.launches++;
     dims[a] = C.ext;
     src = dst;
   }
-  launch_mask_dirichlet(c.stream, C.l2g, C.lat_n, out);
-  c.launches++;
 }
 
 // u(level l) += coef * P coarse(level l-1)
@@ -678,14 +722,13 @@ void op_prolong_add(pmg_ctx& c, int l, const double* coarse, double coef, double
   int dims[3] = {C.ext, C.ext, C.ext};
   const double* src = coarse;
   for (int a = 0; a < c.dim; ++a) {
-    double* dst = c.tbuf[a & 1];
-    launch_ts_axis(c.stream, F.ts, false, F.K, c.dim, dims, a, src, dst);
+    const bool last = a == c.dim - 1;
+    double* dst = last ? u : c.tbuf[a & 1];
+    launch_ts_axis(c.stream, F.ts, false, F.K, c.dim, dims, a, src, dst, last ? 2 : 0, F.l2g, coef);
     c.launches++;
     dims[a] = F.ext;
     src = dst;
   }
-  launch_masked_axpy(c.stream, F.l2g, F.lat_n, coef, src, u);
-  c.launches++;
 }
 
 void op_coarse(pmg_ctx& c, const double* r, double* out) {
@@ -787,17 +830,49 @@ int pcg_device(pmg_ctx& c, const double* f, double tol, int max_iter, double* u,
   launch_copy(c.stream, z, p, n);
   c.launches++;
   op_dot(c, Lf, r, z, s + 0);  // rz
-  for (int k = 1; k <= max_iter; ++k) {
+  // iteration front: Ap, alpha, u += alpha p, r -= alpha Ap, |r| -> host
+  auto front = [&]() {
     op_spmv(c, Lf, p, nullptr, Ap, c.partial);  // Ap and the partials of Ap.p
-    launch_sum_partials(c.stream, c.partial, spmv_blocks(n), s + 1);
+    launch_sum_partials(c.stream, c.partial, spmv_partials(c.dim, c.degree, F.S, F.K), s + 1);
     launch_pcg_scalars(c.stream, 0, s);  // alpha = rz / pAp
     launch_axpy(c.stream, 0.0, s + 2, 1.0, p, u, n);
     launch_axpy(c.stream, 0.0, s + 2, -1.0, Ap, r, n);
     c.launches += 4;
     norm2();
-    read_scalars();
+    ck(cudaMemcpyAsync(c.h_scal, s, 8 * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "scalar D2H");
+  };
+  // iteration back: z = M r, beta, p = z + beta p.  Enqueued before the host
+  // has seen |r|; after the last iteration it only touches z and p.
+  auto back = [&]() {
+    precondition(c, r, z);
+    op_dot(c, Lf, r, z, s + 3);          // rz_next
+    launch_pcg_scalars(c.stream, 1, s);  // beta, rz = rz_next
+    launch_xpay(c.stream, z, 0.0, s + 4, p, n);
+    c.launches += 2;
+  };
+  const bool graphs = c.use_graphs && !c.profiling;
+  if (graphs && c.graph_u != u) {
+    c.capture(c.graph_front, c.graph_front_launches, front);
+    c.capture(c.graph_back, c.graph_back_launches, back);
+    c.graph_u = u;
+  }
+  for (int k = 1; k <= max_iter; ++k) {
+    if (graphs) {
+      c.launch_graph(c.graph_front, c.graph_front_launches);
+    } else {
+      front();
+    }
+    ck(cudaEventRecord(c.ev_norm, c.stream), "cudaEventRecord");
+    if (k < max_iter) {
+      if (graphs)
+        c.launch_graph(c.graph_back, c.graph_back_launches);
+      else
+        back();
+    }
+    ck(cudaEventSynchronize(c.ev_norm), "cudaEventSynchronize");
     if (c.h_scal[7] != 0.0) {
       c.h_scal[7] = 0.0;
+      sync_check(c);
       ck(cudaMemsetAsync(s + 7, 0, sizeof(double), c.stream), "memset");
       throw PmgError(PMG_ERR_DEFINITENESS, "pcg: search direction with nonpositive energy");
     }
@@ -805,11 +880,6 @@ int pcg_device(pmg_ctx& c, const double* f, double tol, int max_iter, double* u,
     history[k] = rn;
     *iters = k;
     if (rn <= tol * r0) return PMG_OK;
-    precondition(c, r, z);
-    op_dot(c, Lf, r, z, s + 3);          // rz_next
-    launch_pcg_scalars(c.stream, 1, s);  // beta, rz = rz_next
-    launch_xpay(c.stream, z, 0.0, s + 4, p, n);
-    c.launches += 2;
   }
   return PMG_ERR_DIVERGENCE;
 }
@@ -870,6 +940,7 @@ int pmg_ctx_create(const pmg_hierarchy_desc* desc, int device, const pmg_comm_de
     }
     ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own_stream;
+    ck(cudaEventCreateWithFlags(&c->ev_norm, cudaEventDisableTiming), "cudaEventCreate");
     build_ctx(*c, *desc);
   } catch (const PmgError& e) {
     g_create_error = e.what();

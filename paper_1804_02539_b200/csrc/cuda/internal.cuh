@@ -58,6 +58,11 @@ struct SpmvArgs {
 };
 void launch_spmv(cudaStream_t s, const SpmvArgs& a);
 int spmv_blocks(long long rows);
+// band row stride per (patch, offset): S, or S rounded up to 256 on levels
+// streamed with TMA bulk copies
+long long spmv_padded_rows(int dim, int degree, long long S);
+// number of dot partials one launch writes
+int spmv_partials(int dim, int degree, long long S, int K);
 
 // ---------------------------------------------------------------- misc kernels
 void launch_fill(cudaStream_t s, double* x, long long n, double v);
@@ -106,14 +111,16 @@ struct TsDev {
   const int* col_row;    // fine rows, ascending
   const double* col_val;
 };
-// one tensor axis pass over K patches: in dims -> out dims (axis changes extent)
+// one tensor axis pass over K patches: in dims -> out dims (axis changes
+// extent).  mode 0 writes; 1 writes with Dirichlet slots zeroed (l2g of the
+// output lattice); 2 adds coef * value on non-Dirichlet slots.
 void launch_ts_axis(cudaStream_t s, const TsDev& ts, bool transpose, int K, int d, const int* in_dims, int axis,
-                    const double* in, double* out);
+                    const double* in, double* out, int mode = 0, const int* l2g = nullptr, double coef = 0.0);
 // final fine write of a prolongation: u[slot] += c * val where l2g >= 0
 void launch_masked_axpy(cudaStream_t s, const int* l2g, long long n, double c, const double* val, double* u);
 void launch_mask_dirichlet(cudaStream_t s, const int* l2g, long long n, double* v);
-void launch_zero_dirichlet_band(cudaStream_t s, int dim, int degree, int ext, long long S, int K, const int* l2g,
-                                double* band);
+void launch_zero_dirichlet_band(cudaStream_t s, int dim, int degree, int ext, long long S, long long Sp, int K,
+                                const int* l2g, double* band);
 // scalar helpers on device: out = num/den ; check energy
 void launch_pcg_scalars(cudaStream_t s, int op, double* scal);
 

@@ -15,10 +15,11 @@
 //
 // Roofline: FP64 tensor cores.  The contraction runs on DMMA
 // (mma.sync.m8n8k4.f64, measured 37.0 TFLOP/s on B200 against 33.6 for DFMA,
-// profiles/fp64_peak_r01.txt).  CTA = 8 warps; warp w owns rows 8w..8w+7 of a
-// 64-row panel and NTC n-tiles of 8 columns; K streams through shared memory
-// in chunks of 16 with cp.async double buffering.  Flops per application =
-// sum_pieces 4 prod(m_a) sum(m_a).
+// profiles/fp64_peak_r01.txt).  CTA = 4 warps; warp w owns rows 8w..8w+7 of a
+// 32-row panel and the 9 n-tiles (72 columns) of the CTA; K streams through
+// shared memory in chunks of 16 through a 3-stage cp.async ring.  Every
+// thread's copy addresses are computed once per CTA.  Flops per application
+// = sum_pieces 4 prod(m_a) sum(m_a).
 #include <cstdint>
 
 #include "internal.cuh"
@@ -27,21 +28,26 @@ namespace pmgcu {
 
 namespace {
 
-constexpr int kBM = 64;        // rows per CTA
-constexpr int kBK = 16;        // k per shared-memory stage
-constexpr int kNTC = 9;        // n-tiles (of 8 columns) per CTA
-constexpr int kBN = 8 * kNTC;  // 72 columns per CTA
-constexpr int kXS = kBK + 4;   // X row stride (doubles): conflict-free A fragments
-constexpr int kBS = 84;        // B row stride: round_up(72, 16) + 4, conflict-free B fragments
+constexpr int kFdThreads = 128;
+constexpr int kBM = 32;          // rows per CTA (4 warps x 8)
+constexpr int kBK = 16;          // k per shared-memory stage
+constexpr int kNTC = 9;          // n-tiles (of 8 columns) per CTA
+constexpr int kBN = 8 * kNTC;    // 72 columns per CTA
+constexpr int kXS = kBK + 4;     // X row stride (doubles): conflict-free A fragments
+constexpr int kBS = 84;          // B row stride: round_up(72, 16) + 4, conflict-free B fragments
+constexpr int kStagesFd = 3;
+constexpr int kXPer = kBM * kBK / kFdThreads;  // 4 X copies per thread and stage
+constexpr int kBPer = kBK * kBN / kFdThreads;  // 9 B copies per thread and stage
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int src_size = pred ? 8 : 0;  // 0 bytes read -> zero fill
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_size));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(pred ? 8 : 0));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all_but_one() { asm volatile("cp.async.wait_group 1;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -49,87 +55,91 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-struct PassCtx {
-  const FdPiece* P;
-  int naxes, in_mode, K, N, m0, m1;
-  long long R, r0, ext, ext2;
-  const double* B;
-  const double* lat_in;
-  const double* work_in;
-};
-
-__device__ __forceinline__ const double* row_ptr(const PassCtx& c, long long r) {
-  if (c.in_mode == FD_IN_WORK) return c.work_in + c.P->work_off + r * c.K;
-  const long long base = c.naxes == 3 ? c.ext * (r % c.m1) + c.ext2 * (r / c.m1) : c.ext * r;
-  return c.lat_in + c.P->lat_base + base;
-}
-
-__device__ __forceinline__ void load_stage(const PassCtx& c, int k0, int n0, double* Xs, double* Bs) {
-  // X: 64 rows x 16 k, 8-byte transfers, zero-filled outside [R) x [K)
-  for (int idx = threadIdx.x; idx < kBM * kBK; idx += kThreads) {
-    const int kk = idx % kBK, rr = idx / kBK;
-    const long long r = c.r0 + rr;
-    const int k = k0 + kk;
-    const bool ok = r < c.R && k < c.K;
-    cp_async8(Xs + rr * kXS + kk, ok ? row_ptr(c, r) + k : c.B, ok);
-  }
-  // B: 16 k x 72 n
-  for (int idx = threadIdx.x; idx < kBK * kBN; idx += kThreads) {
-    const int nn = idx % kBN, kk = idx / kBN;
-    const int k = k0 + kk, n = n0 + nn;
-    const bool ok = k < c.K && n < c.N;
-    cp_async8(Bs + kk * kBS + nn, ok ? c.B + (long long)k * c.N + n : c.B, ok);
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) fd_pass_dmma_kernel(const FdPiece* __restrict__ pieces,
-                                                                const int4* __restrict__ items, int pass,
-                                                                int naxes, int in_mode, int out_mode,
-                                                                const double* __restrict__ lat_in,
-                                                                double* __restrict__ lat_out, double alpha,
-                                                                const double* __restrict__ work_in,
-                                                                double* __restrict__ work_out) {
-  __shared__ __align__(16) double Xs[2][kBM * kXS];
-  __shared__ __align__(16) double Bs[2][kBK * kBS];
+__global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece* __restrict__ pieces,
+                                                                  const int4* __restrict__ items, int pass,
+                                                                  int naxes, int in_mode, int out_mode,
+                                                                  const double* __restrict__ lat_in,
+                                                                  double* __restrict__ lat_out, double alpha,
+                                                                  const double* __restrict__ work_in,
+                                                                  double* __restrict__ work_out) {
+  __shared__ __align__(16) double Xs[kStagesFd][kBM * kXS];
+  __shared__ __align__(16) double Bs[kStagesFd][kBK * kBS];
   const int4 it = items[blockIdx.x];  // (piece, first row, first column, -)
-  PassCtx c;
-  c.P = pieces + it.x;
-  c.naxes = naxes;
-  c.in_mode = in_mode;
+  const FdPiece& P = pieces[it.x];
   const int axis = pass % naxes;
   const int dir = pass / naxes;
-  c.K = c.P->dims[axis];
-  c.N = c.K;
-  c.R = c.P->total / c.K;
-  c.r0 = it.y;
-  c.m0 = c.P->dims[0];
-  c.m1 = c.P->dims[1];
-  c.ext = c.P->ext;
-  c.ext2 = (long long)c.P->ext * c.P->ext;
-  c.B = c.P->B[axis][dir];
-  c.lat_in = lat_in;
-  c.work_in = work_in;
+  const int K = P.dims[axis];
+  const int N = K;
+  const long long R = P.total / K;
+  const long long r0 = it.y;
   const int n0 = it.z;
+  const int m0 = P.dims[0], m1 = P.dims[1];
+  const long long ext = P.ext, ext2 = (long long)P.ext * P.ext;
+  const double* __restrict__ B = P.B[axis][dir];
+  const int tid = threadIdx.x;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // per-thread copy plan: X element (rr, kk) = (tid/16 + 8j, tid%16); B element
+  // (kk, nn) of idx = tid + 128j
+  const int xk = tid % kBK;
+  const double* xsrc[kXPer];
+  bool xrow_ok[kXPer];
+#pragma unroll
+  for (int j = 0; j < kXPer; ++j) {
+    const long long r = r0 + tid / kBK + 8 * j;
+    xrow_ok[j] = r < R;
+    const long long rr = xrow_ok[j] ? r : 0;
+    if (in_mode == FD_IN_WORK)
+      xsrc[j] = work_in + P.work_off + rr * K + xk;
+    else
+      xsrc[j] = lat_in + P.lat_base + (naxes == 3 ? ext * (rr % m1) + ext2 * (rr / m1) : ext * rr) + xk;
+  }
+  int boff[kBPer], bkk[kBPer], bdst[kBPer];
+  bool bn_ok[kBPer];
+#pragma unroll
+  for (int j = 0; j < kBPer; ++j) {
+    const int idx = tid + kFdThreads * j;
+    const int nn = idx % kBN, kk = idx / kBN;
+    bn_ok[j] = n0 + nn < N;
+    bkk[j] = kk;
+    boff[j] = kk * N + n0 + nn;
+    bdst[j] = kk * kBS + nn;
+  }
+  auto load = [&](int stage, int k0) {
+    double* xs = Xs[stage];
+    double* bs = Bs[stage];
+#pragma unroll
+    for (int j = 0; j < kXPer; ++j) {
+      const bool ok = xrow_ok[j] && k0 + xk < K;
+      cp_async8(xs + (tid / kBK + 8 * j) * kXS + xk, ok ? xsrc[j] + k0 : B, ok);
+    }
+#pragma unroll
+    for (int j = 0; j < kBPer; ++j) {
+      const bool ok = bn_ok[j] && k0 + bkk[j] < K;
+      cp_async8(bs + bdst[j], ok ? B + boff[j] + (long long)k0 * N : B, ok);
+    }
+  };
+
+  const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   double acc[kNTC][2];
 #pragma unroll
   for (int j = 0; j < kNTC; ++j) acc[j][0] = acc[j][1] = 0.0;
 
-  const int nstages = (c.K + kBK - 1) / kBK;
-  load_stage(c, 0, n0, Xs[0], Bs[0]);
-  cp_async_commit();
-  for (int s = 0; s < nstages; ++s) {
-    const int cur = s & 1;
-    if (s + 1 < nstages) {
-      load_stage(c, (s + 1) * kBK, n0, Xs[cur ^ 1], Bs[cur ^ 1]);
-      cp_async_commit();
-      cp_async_wait_all_but_one();
-    } else {
-      cp_async_wait_all();
-    }
+  const int nst = (K + kBK - 1) / kBK;
+#pragma unroll
+  for (int s = 0; s < kStagesFd - 1; ++s) {
+    if (s < nst) load(s, s * kBK);
+    cp_async_commit();
+  }
+  for (int s = 0; s < nst; ++s) {
+    const int cur = s % kStagesFd;
+    cp_async_wait<kStagesFd - 2>();
     __syncthreads();
+    {  // prefetch stage s + 2 into the slot freed at s - 1
+      const int nxt = s + kStagesFd - 1;
+      if (nxt < nst) load(nxt % kStagesFd, nxt * kBK);
+      cp_async_commit();
+    }
     const double* xs = Xs[cur] + (warp * 8 + g) * kXS + t;
     const double* bs = Bs[cur] + t * kBS + g;
 #pragma unroll
@@ -138,25 +148,22 @@ __global__ void __launch_bounds__(kThreads) fd_pass_dmma_kernel(const FdPiece* _
 #pragma unroll
       for (int j = 0; j < kNTC; ++j) dmma(acc[j][0], acc[j][1], a, bs[ks * 4 * kBS + j * 8]);
     }
-    __syncthreads();
   }
 
   // epilogue: lane holds rows r0+8w+g, columns n0+8j+2t+{0,1}; Y(r,n) at r + R n
-  const long long r = c.r0 + warp * 8 + g;
-  if (r >= c.R) return;
-  const FdPiece& P = *c.P;
+  const long long r = r0 + warp * 8 + g;
+  if (r >= R) return;
   long long lat_row = 0;
-  if (out_mode >= FD_OUT_LATTICE_SET)
-    lat_row = P.lat_base + (naxes == 3 ? (r % c.m0) + c.ext * (r / c.m0) : r);
-  const long long lat_stride = naxes == 3 ? c.ext2 : c.ext;
+  if (out_mode >= FD_OUT_LATTICE_SET) lat_row = P.lat_base + (naxes == 3 ? (r % m0) + ext * (r / m0) : r);
+  const long long lat_stride = naxes == 3 ? ext2 : ext;
 #pragma unroll
   for (int j = 0; j < kNTC; ++j) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int n = n0 + j * 8 + 2 * t + i;
-      if (n >= c.N) continue;
+      if (n >= N) continue;
       const double v = acc[j][i];
-      const long long o = r + c.R * n;
+      const long long o = r + R * n;
       switch (out_mode) {
         case FD_OUT_WORK:
           work_out[P.work_off + o] = v;
@@ -185,8 +192,8 @@ void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, in
                     int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
                     const double* work_in, double* work_out) {
   if (nitems == 0) return;
-  fd_pass_dmma_kernel<<<nitems, kThreads, 0, s>>>(pieces, items, pass, naxes, in_mode, out_mode, lat_in, lat_out,
-                                                  alpha, work_in, work_out);
+  fd_pass_dmma_kernel<<<nitems, kFdThreads, 0, s>>>(pieces, items, pass, naxes, in_mode, out_mode, lat_in, lat_out,
+                                                    alpha, work_in, work_out);
 }
 
 }  // namespace pmgcu

@@ -233,8 +233,12 @@ __global__ void coarse_scatter_kernel(const int* __restrict__ l2g, long long n, 
 
 // One tensor axis of the two-scale kronecker product over K patches
 // (apply_along_axis(TwoScale), tensor.cpp:52-102); each thread one output.
+// mode 0: out = s; 1: out = s on non-Dirichlet slots, 0 elsewhere (last
+// restriction pass); 2: out += coef s on non-Dirichlet slots (last
+// prolongation pass, u += c P coarse).
 __global__ void ts_axis_kernel(TsDev ts, int transpose, int K, int d, int in0, int in1, int in2, int axis,
-                               const double* __restrict__ in, double* __restrict__ out) {
+                               const double* __restrict__ in, double* __restrict__ out, int mode,
+                               const int* __restrict__ l2g, double coef) {
   int dims_in[3] = {in0, in1, in2};
   int dims_out[3] = {in0, in1, in2};
   dims_out[axis] = transpose ? ts.coarse_dim : ts.fine_dim;
@@ -260,7 +264,12 @@ __global__ void ts_axis_kernel(TsDev ts, int transpose, int K, int d, int in0, i
     } else {
       for (int q = ts.col_off[j]; q < ts.col_off[j + 1]; ++q) s = fma(ts.col_val[q], src[(long long)ts.col_row[q] * inner], s);
     }
-    out[idx] = s;
+    if (mode == 0)
+      out[idx] = s;
+    else if (mode == 1)
+      out[idx] = l2g[idx] >= 0 ? s : 0.0;
+    else if (l2g[idx] >= 0)
+      out[idx] += coef * s;
   }
 }
 
@@ -277,17 +286,23 @@ __global__ void mask_dirichlet_kernel(const int* __restrict__ l2g, long long n, 
   if (l2g[i] < 0) v[i] = 0.0;
 }
 
-__global__ void zero_dirichlet_band_kernel(int dim, int degree, int ext, long long S, int K, const int* __restrict__ l2g,
-                                           double* __restrict__ band) {
+// zero Dirichlet rows/columns and the columns leaving the lattice; padding
+// rows r in [S, Sp) are zeroed too
+__global__ void zero_dirichlet_band_kernel(int dim, int degree, int ext, long long S, long long Sp, int K,
+                                           const int* __restrict__ l2g, double* __restrict__ band) {
   const int W = 2 * degree + 1;
   const int O = dim == 2 ? W * W : W * W * W;
-  const long long total = (long long)K * O * S;
+  const long long total = (long long)K * O * Sp;
   for (long long idx = blockIdx.x * (long long)kThreads + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * kThreads) {
-    const long long k = idx / (O * S);
-    const long long rem = idx - k * O * S;
-    const int o = int(rem / S);
-    const long long r = rem - (long long)o * S;
+    const long long k = idx / (O * Sp);
+    const long long rem = idx - k * O * Sp;
+    const int o = int(rem / Sp);
+    const long long r = rem - (long long)o * Sp;
+    if (r >= S) {
+      band[idx] = 0.0;
+      continue;
+    }
     const int i0 = int(r % ext), i1 = int((r / ext) % ext), i2 = dim == 3 ? int(r / ((long long)ext * ext)) : 0;
     const int d0 = o % W - degree, d1 = (o / W) % W - degree, d2 = dim == 3 ? o / (W * W) - degree : 0;
     const int j0 = i0 + d0, j1 = i1 + d1, j2 = i2 + d2;
@@ -384,14 +399,14 @@ void launch_coarse(cudaStream_t s, const int* rep_off, const int* rep_slot, cons
   coarse_scatter_kernel<<<grid_for(lat_n), kThreads, 0, s>>>(l2g, lat_n, x, out);
 }
 void launch_ts_axis(cudaStream_t s, const TsDev& ts, bool transpose, int K, int d, const int* in_dims, int axis,
-                    const double* in, double* out) {
+                    const double* in, double* out, int mode, const int* l2g, double coef) {
   long long per_out = 1;
   for (int a = 0; a < d; ++a) per_out *= (a == axis ? (transpose ? ts.coarse_dim : ts.fine_dim) : in_dims[a]);
   const long long total = per_out * K;
   long long g = (total + kThreads - 1) / kThreads;
   if (g > 148LL * 32) g = 148LL * 32;
   ts_axis_kernel<<<int(g < 1 ? 1 : g), kThreads, 0, s>>>(ts, transpose ? 1 : 0, K, d, in_dims[0], in_dims[1],
-                                                         d == 3 ? in_dims[2] : 1, axis, in, out);
+                                                         d == 3 ? in_dims[2] : 1, axis, in, out, mode, l2g, coef);
 }
 void launch_masked_axpy(cudaStream_t s, const int* l2g, long long n, double c, const double* val, double* u) {
   if (n > 0) masked_axpy_kernel<<<grid_for(n), kThreads, 0, s>>>(l2g, n, c, val, u);
@@ -399,9 +414,9 @@ void launch_masked_axpy(cudaStream_t s, const int* l2g, long long n, double c, c
 void launch_mask_dirichlet(cudaStream_t s, const int* l2g, long long n, double* v) {
   if (n > 0) mask_dirichlet_kernel<<<grid_for(n), kThreads, 0, s>>>(l2g, n, v);
 }
-void launch_zero_dirichlet_band(cudaStream_t s, int dim, int degree, int ext, long long S, int K, const int* l2g,
-                                double* band) {
-  zero_dirichlet_band_kernel<<<148 * 32, kThreads, 0, s>>>(dim, degree, ext, S, K, l2g, band);
+void launch_zero_dirichlet_band(cudaStream_t s, int dim, int degree, int ext, long long S, long long Sp, int K,
+                                const int* l2g, double* band) {
+  zero_dirichlet_band_kernel<<<148 * 32, kThreads, 0, s>>>(dim, degree, ext, S, Sp, K, l2g, band);
 }
 void launch_pcg_scalars(cudaStream_t s, int op, double* scal) { pcg_scalars_kernel<<<1, 32, 0, s>>>(op, scal); }
 

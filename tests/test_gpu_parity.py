@@ -140,9 +140,11 @@ def test_pcg_matches_oracle(setup):
     assert rep.iterations == len(hist_ref) - 1
     hist = np.array(rep.residual_history)
     diff = np.abs(hist - hist_ref)
-    assert np.all(diff <= 1e-10 * hist_ref + 1e-12 * hist_ref[0])
+    info = (f"max |dr|/r0 = {diff.max() / hist_ref[0]:.2e}, max |dr|/r_k = {(diff / hist_ref).max():.2e}, "
+            f"final rel res {hist_ref[-1] / hist_ref[0]:.3e}")
+    assert np.all(diff <= 1e-10 * hist_ref + 1e-12 * hist_ref[0]), info
     early = hist_ref >= 1e-4 * hist_ref[0]
-    assert np.all(diff[early] <= 1e-10 * hist_ref[early])
+    assert np.all(diff[early] <= 1e-10 * hist_ref[early]), info
     # yardstick: the reference's own serial vs 2-rank parallel solve differ by
     # the same kind of reassociation; the GPU stays within 20x of that spread
     if h.num_patches >= 2:
