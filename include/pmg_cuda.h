@@ -34,16 +34,34 @@ typedef struct pmg_vec pmg_vec;
 
 enum { PMG_ACCUMULATED = 0, PMG_DISTRIBUTED = 1 };
 
-/* Multi-GPU placement: this context owns patches [patch_begin, patch_end) of
- * the hierarchy (contiguous_partition, parallel.cpp:181-198).  nccl_comm is an
- * ncclComm_t spanning `size` ranks (one GPU each) or NULL when size == 1. */
+/* In-process rank hub: R ranks as threads of one process exchanging through
+ * host-mediated device copies (the reference's InProcHub, parallel.hpp:70-113). */
+typedef struct pmg_hub pmg_hub;
+
+enum { PMG_TRANSPORT_NONE = 0, PMG_TRANSPORT_NCCL = 1, PMG_TRANSPORT_HUB = 2 };
+
+/* Multi-GPU placement: this context owns patches [patch_begin, patch_end), the
+ * contiguous_partition block of `rank` (parallel.cpp:181-198).  With size > 1
+ * the ranks exchange interface sums, scalar reductions and the coarse
+ * residual over `transport`: NCCL (one process per GPU; every rank passes the
+ * same nccl_id from pmg_nccl_unique_id) or an in-process hub. */
 typedef struct {
   int rank;
   int size;
   int patch_begin;
   int patch_end;
-  void* nccl_comm;
+  int transport;               /* PMG_TRANSPORT_* */
+  unsigned char nccl_id[128];  /* ncclUniqueId */
+  pmg_hub* hub;
 } pmg_comm_desc;
+
+int pmg_nccl_unique_id(unsigned char out[128]);
+int pmg_hub_create(int ranks, pmg_hub** out);
+void pmg_hub_destroy(pmg_hub* hub);
+/* wake every rank blocked in the hub with a TransportError (run_ranks poison) */
+int pmg_hub_poison(pmg_hub* hub, const char* reason);
+/* payload bytes this rank pushed to peers (Communicator::bytes_sent) */
+int pmg_comm_bytes(pmg_ctx* ctx, uint64_t* out);
 
 /* Upload one hierarchy (Hierarchy, multigrid.hpp:42-75) to `device`.
  * comm == NULL: single GPU owning every patch. */

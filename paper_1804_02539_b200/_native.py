@@ -45,6 +45,13 @@ class PmgHierarchyDesc(C.Structure):
     ]
 
 
+class PmgCommDesc(C.Structure):
+    _fields_ = [("rank", C.c_int), ("size", C.c_int), ("patch_begin", C.c_int), ("patch_end", C.c_int),
+                ("transport", C.c_int), ("nccl_id", C.c_ubyte * 128), ("hub", C.c_void_p)]
+
+
+PMG_TRANSPORT_NONE, PMG_TRANSPORT_NCCL, PMG_TRANSPORT_HUB = 0, 1, 2
+
 PMG_OK = 0
 PMG_ERR_CONFIG = 2
 PMG_ERR_DIVERGENCE = 3
@@ -112,6 +119,7 @@ CUDA_SYMBOLS = [
     "pmg_coarse_solve", "pmg_dot", "pmg_axpy", "pmg_xpay",
     "pmg_mg_cycle", "pmg_precondition", "pmg_pcg_solve_device", "pmg_pcg_solve",
     "pmg_kernel_stats", "pmg_synchronize", "pmg_profile", "pmg_profile_read",
+    "pmg_nccl_unique_id", "pmg_hub_create", "pmg_hub_destroy", "pmg_hub_poison", "pmg_comm_bytes",
 ]
 
 
@@ -126,7 +134,13 @@ def cuda_lib():
         lib = C.CDLL(str(path))
         for name in CUDA_SYMBOLS:
             getattr(lib, name)  # every declared entry point must exist
-        _sig(lib, "pmg_ctx_create", C.c_int, [C.POINTER(PmgHierarchyDesc), C.c_int, _vp, C.POINTER(_vp)])
+        _sig(lib, "pmg_ctx_create", C.c_int, [C.POINTER(PmgHierarchyDesc), C.c_int, C.POINTER(PmgCommDesc),
+                                              C.POINTER(_vp)])
+        _sig(lib, "pmg_nccl_unique_id", C.c_int, [C.POINTER(C.c_ubyte * 128)])
+        _sig(lib, "pmg_hub_create", C.c_int, [C.c_int, C.POINTER(_vp)])
+        _sig(lib, "pmg_hub_destroy", None, [_vp])
+        _sig(lib, "pmg_hub_poison", C.c_int, [_vp, C.c_char_p])
+        _sig(lib, "pmg_comm_bytes", C.c_int, [_vp, C.POINTER(C.c_uint64)])
         _sig(lib, "pmg_ctx_destroy", None, [_vp])
         _sig(lib, "pmg_last_error", C.c_char_p, [_vp])
         _sig(lib, "pmg_ctx_info", C.c_int, [_vp, C.c_int, C.POINTER(C.c_int64)])

@@ -65,13 +65,26 @@ def _need(v, cls, level):
 
 
 class GpuBackend:
-    def __init__(self, hierarchy: Hierarchy, device: int = 0):
+    """One rank's backend.  comm=None: a single GPU owning every patch;
+    otherwise a PmgCommDesc (see parallel.py) placing this context on its
+    contiguous patch block with an NCCL or in-process-hub transport."""
+
+    def __init__(self, hierarchy: Hierarchy, device: int = 0, comm: N.PmgCommDesc | None = None):
         self._lib = N.cuda_lib()
         self.h = hierarchy
+        self.comm = comm
+        self.rank = comm.rank if comm is not None else 0
+        self.size = comm.size if comm is not None else 1
         ctx = C.c_void_p()
-        rc = self._lib.pmg_ctx_create(C.byref(hierarchy.desc), device, None, C.byref(ctx))
+        rc = self._lib.pmg_ctx_create(C.byref(hierarchy.desc), device, C.byref(comm) if comm is not None else None,
+                                      C.byref(ctx))
         raise_for(rc, self._lib.pmg_last_error(None).decode())
         self._ctx = ctx
+
+    def comm_bytes(self) -> int:
+        n = C.c_uint64()
+        self._check(self._lib.pmg_comm_bytes(self._ctx, C.byref(n)))
+        return n.value
 
     def close(self):
         if getattr(self, "_ctx", None):

@@ -25,6 +25,8 @@
 #include <vector>
 
 #include "../../../include/pmg_cuda.h"
+#include "../common/rank_plan.hpp"
+#include "comm.cuh"
 #include "internal.cuh"
 
 using namespace pmgcu;
@@ -48,19 +50,28 @@ struct DevLevel {
   unsigned char* owner = nullptr;
   int* rep_off = nullptr;
   int* rep_slot = nullptr;
-  int* goff = nullptr;
-  int* gslot = nullptr;
-  int ngroups = 0;
+  // interface dofs of this rank (pmgplan::RankPlan): local replicas, fold
+  // sources, exchange buffers, partial and total sums
+  int n_iface = 0;
+  int *if_rep_off = nullptr, *if_rep_slot = nullptr, *if_comb_off = nullptr, *if_comb_src = nullptr;
+  double *if_tloc = nullptr, *if_t = nullptr;
+  int* if_send_idx = nullptr;
+  int n_send = 0, n_recv = 0;
+  double *if_send = nullptr, *if_recv = nullptr;
+  std::vector<Peer> peers;
   // interior FD
   FdPiece* d_int = nullptr;
   int n_int = 0;
   int4* int_items[6] = {};
   int n_int_items[6] = {};
   std::vector<std::array<int, 3>> int_dims;  // host copy for flop counts
+  bool int_small = false, face_small = false;  // whole solve per CTA in shared memory
+  long long int_max_total = 0, face_max_total = 0;
+  int int_max_dim = 0, face_max_dim = 0;
   // faces
   FdPiece* d_face = nullptr;
   int n_face = 0;
-  int* face_dof_g = nullptr;
+  int* face_iface = nullptr;  // face piece dofs as interface indices
   long long face_ndof = 0;
   int4* face_items[4] = {};
   int n_face_items[4] = {};
@@ -69,8 +80,8 @@ struct DevLevel {
   int n_edges = 0;
   int2* edge_items = nullptr;
   int n_edge_items = 0;
-  int* edge_dof_g = nullptr;
-  int* vert_g = nullptr;
+  int* edge_iface = nullptr;
+  int* vert_iface = nullptr;
   double* vert_scalar = nullptr;
   int n_verts = 0;
   // two-scale factor from level-1 (level >= 1)
@@ -83,9 +94,18 @@ struct DevLevel {
 
 }  // namespace
 
+struct pmg_hub {
+  explicit pmg_hub(int r) : hub(r) {}
+  Hub hub;
+};
+
 struct pmg_ctx {
   int device = 0;
   int dim = 0, degree = 0, K_global = 0, pb = 0, pe = 0, nl = 0;
+  int rank = 0, size = 1;
+  std::unique_ptr<Transport> comm;  // null when size == 1
+  double* rank_buf = nullptr;       // size doubles (scalar all-gathers)
+  double* coarse_parts = nullptr;   // size x n0 (coarse gather on rank 0)
   pmg_cycle_params prm{};
   std::vector<DevLevel> lv;
   double* work[2] = {nullptr, nullptr};
@@ -339,15 +359,34 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   L.rep_off = c.upload(rep_off);
   L.rep_slot = c.upload(rep_slot);
   L.owner = c.upload(owner);
-  std::vector<int> goff(1, 0), gslot;
-  for (long long g = 0; g < L.N; ++g)
-    if (rep_off[g + 1] - rep_off[g] >= 2) {
-      for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) gslot.push_back(rep_slot[q]);
-      goff.push_back(int(gslot.size()));
+  // ---- interface dofs and the exchange plan of this rank (RankLayout, parallel.cpp:200-237)
+  const pmgplan::Partition part = pmgplan::contiguous(D.num_patches, c.size);
+  const pmgplan::RankPlan plan = pmgplan::build(l2g_all, D.num_patches, S, L.N, part, c.rank);
+  L.n_iface = int(plan.iface_g.size());
+  L.if_rep_off = c.upload(plan.rep_off);
+  L.if_rep_slot = c.upload(plan.rep_slot);
+  L.if_comb_off = c.upload(plan.comb_off);
+  L.if_comb_src = c.upload(plan.comb_src);
+  L.if_tloc = c.alloc<double>(size_t(L.n_iface));
+  L.if_t = c.alloc<double>(size_t(L.n_iface));
+  std::vector<int> send_idx;
+  for (const auto& nb : plan.neighbors) send_idx.insert(send_idx.end(), nb.iface.begin(), nb.iface.end());
+  L.n_send = L.n_recv = int(send_idx.size());
+  L.if_send_idx = c.upload(send_idx);
+  L.if_send = c.alloc<double>(size_t(L.n_send));
+  L.if_recv = c.alloc<double>(size_t(L.n_recv));
+  {
+    size_t off = 0;
+    for (const auto& nb : plan.neighbors) {
+      L.peers.push_back(Peer{nb.rank, L.if_send + off, nb.iface.size(), L.if_recv + off, nb.iface.size()});
+      off += nb.iface.size();
     }
-  L.ngroups = int(goff.size()) - 1;
-  L.goff = c.upload(goff);
-  L.gslot = c.upload(gslot);
+  }
+  auto iface_of = [&](int g) {
+    const int i = plan.iface_of_g[g];
+    if (i < 0) throw PmgError(PMG_ERR_DOMAIN, "interface piece dof is not shared");
+    return i;
+  };
 
   // ---- pieces
   std::map<const double*, std::pair<const double*, const double*>> vmats;  // V -> (Bfwd, Bbwd)
@@ -453,7 +492,7 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
       fp.work_off = work_face;
       work_face += fp.total;
       fp.diag = diag_of(pc.diag, fp.total);
-      for (int64_t q = 0; q < pc.ndofs; ++q) face_dofs.push_back(pc.dofs[q]);
+      for (int64_t q = 0; q < pc.ndofs; ++q) face_dofs.push_back(iface_of(pc.dofs[q]));
       h_face.push_back(fp);
     } else if (pc.kind == PMG_PIECE_EDGE) {
       if (pc.chol_dim != pc.ndofs) throw PmgError(PMG_ERR_DOMAIN, "piece smoother: local vector size mismatch");
@@ -470,19 +509,23 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
         linvs[key] = dinv;
       }
       h_edges.push_back(EdgePiece{int(pc.ndofs), (long long)edge_dofs.size(), dinv});
-      for (int64_t q = 0; q < pc.ndofs; ++q) edge_dofs.push_back(pc.dofs[q]);
+      for (int64_t q = 0; q < pc.ndofs; ++q) edge_dofs.push_back(iface_of(pc.dofs[q]));
     } else {
-      vert_g.push_back(pc.dofs[0]);
+      vert_g.push_back(iface_of(pc.dofs[0]));
       vert_scalar.push_back(pc.scalar);
     }
   }
-  (void)maxdim_int;
-  (void)maxdim_face;
+  for (const auto& fp : h_int) L.int_max_total = std::max(L.int_max_total, fp.total);
+  for (const auto& fp : h_face) L.face_max_total = std::max(L.face_max_total, fp.total);
+  L.int_max_dim = maxdim_int;
+  L.face_max_dim = maxdim_face;
+  L.int_small = 2 * L.int_max_total + (long long)maxdim_int * maxdim_int <= kFdSmallDoubles;
+  L.face_small = 2 * L.face_max_total + (long long)maxdim_face * maxdim_face <= kFdSmallDoubles;
   L.n_int = int(h_int.size());
   L.d_int = c.upload(h_int);
   L.n_face = int(h_face.size());
   L.d_face = c.upload(h_face);
-  L.face_dof_g = c.upload(face_dofs);
+  L.face_iface = c.upload(face_dofs);
   L.face_ndof = (long long)face_dofs.size();
   L.n_edges = int(h_edges.size());
   L.d_edges = c.upload(h_edges);
@@ -493,9 +536,9 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
     L.n_edge_items = int(ei.size());
     L.edge_items = c.upload(ei);
   }
-  L.edge_dof_g = c.upload(edge_dofs);
+  L.edge_iface = c.upload(edge_dofs);
   L.n_verts = int(vert_g.size());
-  L.vert_g = c.upload(vert_g);
+  L.vert_iface = c.upload(vert_g);
   L.vert_scalar = c.upload(vert_scalar);
   // CTA work items of every pass: (piece, row panel, column panel)
   auto make_items = [&](const std::vector<FdPiece>& ps, int naxes, int4** items, int* counts) {
@@ -594,6 +637,8 @@ void build_ctx(pmg_ctx& c, const pmg_hierarchy_desc& D) {
   c.Ainv = c.upload(spd_inverse(c.n0, D.coarse_L));
   c.coarse_rhs = c.alloc<double>(size_t(c.n0));
   c.coarse_x = c.alloc<double>(size_t(c.n0));
+  c.rank_buf = c.alloc<double>(size_t(c.size));
+  c.coarse_parts = c.alloc<double>(size_t(c.size) * std::max(c.n0, 1));
   long long maxlat = 0;
   for (auto& L : c.lv) maxlat = std::max(maxlat, L.lat_n);
   c.partial_n = dot_blocks(maxlat);
@@ -664,13 +709,36 @@ double fd_pass_flops(const DevLevel& L, const std::vector<std::array<int, 3>>& d
   return f;
 }
 
+// Sigma on the interface dofs of a distributed vector r: this rank's replica
+// partials, the neighbour exchange, and the ascending-rank fold into L.if_t.
+void op_iface_sum(pmg_ctx& c, int l, const double* r) {
+  DevLevel& L = c.lv[l];
+  launch_iface_partial(c.stream, L.n_iface, L.if_rep_off, L.if_rep_slot, r, L.if_tloc);
+  if (L.n_iface) c.launches++;
+  if (c.size > 1) {
+    launch_iface_pack(c.stream, L.n_send, L.if_send_idx, L.if_tloc, L.if_send);
+    if (L.n_send) c.launches++;
+    c.comm->exchange(c.stream, L.peers);
+  }
+  launch_iface_combine(c.stream, L.n_iface, L.if_comb_off, L.if_comb_src, L.if_tloc, L.if_recv, L.if_t);
+  if (L.n_iface) c.launches++;
+}
+
 // smooth: interior FD, faces, edges + vertices.  out_mode SET: out = alpha z
 // on every piece slot; ADD: out += alpha z.
 void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double alpha) {
   const DevLevel& L = c.lv[l];
   const int d = c.dim;
   const int np = 2 * d;
-  for (int pass = 0; pass < np; ++pass) {
+  if (L.int_small) {
+    double flops = 0.0;
+    for (int pass = 0; pass < np; ++pass) flops += fd_pass_flops(L, L.int_dims, d, pass);
+    TimedScope ts(c, 1, l, flops);
+    launch_fd_small(c.stream, L.d_int, L.n_int, d, L.int_max_total, L.int_max_dim, FD_IN_LATTICE,
+                    add ? FD_OUT_LATTICE_ADD : FD_OUT_LATTICE_SET, r, out, alpha, nullptr, nullptr);
+    if (L.n_int) c.launches++;
+  }
+  for (int pass = 0; pass < np && !L.int_small; ++pass) {
     const int in_mode = pass == 0 ? FD_IN_LATTICE : FD_IN_WORK;
     int out_mode = FD_OUT_WORK;
     if (pass == d - 1) out_mode = FD_OUT_WORK_DIAG;
@@ -680,29 +748,54 @@ void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double
                    alpha, c.work[(pass + 1) & 1], c.work[pass & 1]);
     if (L.n_int_items[pass]) c.launches++;
   }
+  // interface pieces act on the summed residual: Sigma over every replica
+  // (all ranks), then each rank solves the pieces it touches and writes its
+  // local replicas (ParallelBackend::smooth = accumulate(apply_pieces(r)),
+  // parallel.cpp:353-355, with the sum taken before the linear piece solves)
+  TimedScope ts_iface(c, 3, l, 0.0);
+  op_iface_sum(c, l, r);
   if (d == 3 && L.n_face > 0) {
-    launch_gather_sum(c.stream, L.face_dof_g, L.face_ndof, L.rep_off, L.rep_slot, r, c.face_buf[1]);
+    launch_gather_t(c.stream, L.face_ndof, L.face_iface, L.if_t, c.face_buf[1]);
     c.launches++;
-    for (int pass = 0; pass < 4; ++pass) {
-      const int out_mode = pass == 1 ? FD_OUT_WORK_DIAG : FD_OUT_WORK;
-      launch_fd_pass(c.stream, L.d_face, L.face_items[pass], L.n_face_items[pass], pass, 2, FD_IN_WORK, out_mode,
-                     nullptr, nullptr, 0.0, c.face_buf[(pass + 1) & 1], c.face_buf[pass & 1]);
+    const double* res = c.face_buf[1];
+    if (L.face_small) {
+      launch_fd_small(c.stream, L.d_face, L.n_face, 2, L.face_max_total, L.face_max_dim, FD_IN_WORK, FD_OUT_WORK,
+                      nullptr, nullptr, 0.0, c.face_buf[1], c.face_buf[0]);
       c.launches++;
+      res = c.face_buf[0];
+    } else {
+      for (int pass = 0; pass < 4; ++pass) {
+        const int out_mode = pass == 1 ? FD_OUT_WORK_DIAG : FD_OUT_WORK;
+        launch_fd_pass(c.stream, L.d_face, L.face_items[pass], L.n_face_items[pass], pass, 2, FD_IN_WORK, out_mode,
+                       nullptr, nullptr, 0.0, c.face_buf[(pass + 1) & 1], c.face_buf[pass & 1]);
+        c.launches++;
+      }
     }
-    launch_scatter(c.stream, L.face_dof_g, L.face_ndof, L.rep_off, L.rep_slot, c.face_buf[1], out, add ? 1 : 0, alpha);
+    launch_scatter_iface(c.stream, L.face_ndof, L.face_iface, L.if_rep_off, L.if_rep_slot, res, out, add ? 1 : 0,
+                         alpha);
     c.launches++;
   }
   if (L.n_edges + L.n_verts > 0) {
-    launch_edges_vertices(c.stream, L.d_edges, L.edge_items, L.n_edge_items, L.edge_dof_g, L.vert_g, L.vert_scalar,
-                          L.n_verts, L.rep_off, L.rep_slot, r, out, add ? 1 : 0, alpha);
+    launch_edges_vertices(c.stream, L.d_edges, L.edge_items, L.n_edge_items, L.edge_iface, L.vert_iface,
+                          L.vert_scalar, L.n_verts, L.if_rep_off, L.if_rep_slot, L.if_t, out, add ? 1 : 0, alpha);
     c.launches++;
   }
 }
+
+// one-pass tensor transfers for 2D and for small 3D lattices; large 3D
+// lattices keep the axis-by-axis passes (fewer redundant loads)
+bool fused_transfer(const pmg_ctx& c, const DevLevel& F) { return c.dim == 2 || F.S <= 40000; }
 
 // restriction level l -> l-1 on distributed shares; out coarse (dist)
 void op_restrict(pmg_ctx& c, int l, const double* r, double* out) {
   const DevLevel& F = c.lv[l];
   const DevLevel& C = c.lv[l - 1];
+  TimedScope ts(c, 2, l, 0.0);
+  if (fused_transfer(c, F)) {
+    launch_restrict_fused(c.stream, F.ts, F.K, c.dim, F.ext, C.ext, r, out, C.l2g);
+    c.launches++;
+    return;
+  }
   int dims[3] = {F.ext, F.ext, F.ext};
   const double* src = r;
   for (int a = 0; a < c.dim; ++a) {
@@ -719,6 +812,12 @@ void op_restrict(pmg_ctx& c, int l, const double* r, double* out) {
 void op_prolong_add(pmg_ctx& c, int l, const double* coarse, double coef, double* u) {
   const DevLevel& F = c.lv[l];
   const DevLevel& C = c.lv[l - 1];
+  TimedScope ts(c, 2, l, 0.0);
+  if (fused_transfer(c, F)) {
+    launch_prolong_fused(c.stream, F.ts, F.K, c.dim, F.ext, C.ext, coarse, coef, u, F.l2g);
+    c.launches++;
+    return;
+  }
   int dims[3] = {C.ext, C.ext, C.ext};
   const double* src = coarse;
   for (int a = 0; a < c.dim; ++a) {
@@ -731,28 +830,57 @@ void op_prolong_add(pmg_ctx& c, int l, const double* coarse, double coef, double
   }
 }
 
+// coarse_solve (parallel.cpp:411-422): the global coarse residual is the sum
+// of every replica share; on several ranks the per-rank partials go to rank 0,
+// which sums them in ascending rank order, solves, and broadcasts the result
 void op_coarse(pmg_ctx& c, const double* r, double* out) {
   const DevLevel& L = c.lv[0];
-  launch_coarse(c.stream, L.rep_off, L.rep_slot, L.l2g, c.n0, L.lat_n, c.Ainv, r, c.coarse_rhs, c.coarse_x, out);
-  c.launches += c.n0 > 0 ? 3 : 1;
+  TimedScope ts(c, 5, 0, 0.0);
+  launch_coarse_gather(c.stream, L.rep_off, L.rep_slot, c.n0, r, c.coarse_rhs);
+  c.launches++;
+  if (c.size > 1) {
+    c.comm->gather(c.stream, c.coarse_rhs, c.coarse_parts, size_t(c.n0), 0);
+    if (c.rank == 0) {
+      launch_sum_ranks(c.stream, c.coarse_parts, c.size, c.n0, c.coarse_rhs);
+      c.launches++;
+    }
+  }
+  if (c.rank == 0) {
+    launch_coarse_gemv(c.stream, c.Ainv, c.n0, c.coarse_rhs, c.coarse_x);
+    c.launches++;
+  }
+  if (c.size > 1) c.comm->broadcast(c.stream, c.coarse_x, size_t(c.n0), 0);
+  launch_coarse_scatter(c.stream, L.l2g, L.lat_n, c.coarse_x, out);
+  c.launches++;
 }
 
-// dot(dist a, acc b) into device scalar slot
+// dot(dist a, acc b) into a device scalar, reduced over ranks in ascending
+// rank order (Communicator::allreduce_sum, parallel.cpp:21-28)
 void op_dot(pmg_ctx& c, int l, const double* a, const double* b, double* dst) {
   const DevLevel& L = c.lv[l];
+  TimedScope ts(c, 4, l, 0.0);
   launch_dot_partial(c.stream, a, b, L.lat_n, c.partial);
   launch_sum_partials(c.stream, c.partial, dot_blocks(L.lat_n), dst);
   c.launches += 2;
+  if (c.size > 1) {
+    c.comm->allgather(c.stream, dst, c.rank_buf, 1);
+    launch_sum_ranks(c.stream, c.rank_buf, c.size, 1, dst);
+    c.launches++;
+  }
 }
 
+// accumulate (parallel.cpp:306-337): out = r with every interface replica
+// replaced by the interface total
 void op_accumulate(pmg_ctx& c, int l, const double* r, double* out) {
-  const DevLevel& L = c.lv[l];
+  DevLevel& L = c.lv[l];
+  TimedScope ts(c, 4, l, 0.0);
+  op_iface_sum(c, l, r);
   if (out != r) {
     launch_copy(c.stream, r, out, L.lat_n);
     c.launches++;
   }
-  launch_group_sum(c.stream, L.goff, L.gslot, L.ngroups, r == out ? out : r, out);
-  if (L.ngroups) c.launches++;
+  launch_iface_scatter(c.stream, L.n_iface, L.if_rep_off, L.if_rep_slot, L.if_t, out);
+  if (L.n_iface) c.launches++;
 }
 
 // mg_cycle_generic (multigrid.hpp:120-141) on the ctx workspace.
@@ -834,6 +962,11 @@ int pcg_device(pmg_ctx& c, const double* f, double tol, int max_iter, double* u,
   auto front = [&]() {
     op_spmv(c, Lf, p, nullptr, Ap, c.partial);  // Ap and the partials of Ap.p
     launch_sum_partials(c.stream, c.partial, spmv_partials(c.dim, c.degree, F.S, F.K), s + 1);
+    if (c.size > 1) {  // pAp over all ranks, ascending rank order
+      c.comm->allgather(c.stream, s + 1, c.rank_buf, 1);
+      launch_sum_ranks(c.stream, c.rank_buf, c.size, 1, s + 1);
+      c.launches++;
+    }
     launch_pcg_scalars(c.stream, 0, s);  // alpha = rz / pAp
     launch_axpy(c.stream, 0.0, s + 2, 1.0, p, u, n);
     launch_axpy(c.stream, 0.0, s + 2, -1.0, Ap, r, n);
@@ -893,6 +1026,9 @@ int guarded(pmg_ctx* c, F&& f) {
   } catch (const PmgError& e) {
     if (c) c->err = e.what();
     return e.code;
+  } catch (const TransportFailure& e) {
+    if (c) c->err = e.what();
+    return PMG_ERR_TRANSPORT;
   } catch (const std::exception& e) {
     if (c) c->err = e.what();
     return PMG_ERR_GENERIC;
@@ -932,11 +1068,26 @@ int pmg_ctx_create(const pmg_hierarchy_desc* desc, int device, const pmg_comm_de
     ck(cudaSetDevice(device), "cudaSetDevice");
     if (comm) {
       need(comm->size >= 1 && comm->rank >= 0 && comm->rank < comm->size, PMG_ERR_CONFIG, "bad rank description");
-      need(comm->patch_begin >= 0 && comm->patch_end <= desc->num_patches && comm->patch_begin < comm->patch_end,
-           PMG_ERR_CONFIG, "bad patch range");
-      need(comm->size == 1, PMG_ERR_CONFIG, "multi-rank contexts need the exchange layer (pmg_comm_desc.size > 1)");
+      need(comm->size <= desc->num_patches && comm->size <= 64, PMG_ERR_CONFIG, "partition: bad rank count");
+      // the exchange plans assume contiguous_partition (parallel.cpp:181-198)
+      const pmgplan::Partition part = pmgplan::contiguous(desc->num_patches, comm->size);
+      need(comm->patch_begin == part.patch_begin[comm->rank] && comm->patch_end == part.patch_begin[comm->rank + 1],
+           PMG_ERR_CONFIG, "patch range is not the contiguous partition block of this rank");
+      c->rank = comm->rank;
+      c->size = comm->size;
       c->pb = comm->patch_begin;
       c->pe = comm->patch_end;
+      if (comm->size > 1) {
+        if (comm->transport == PMG_TRANSPORT_NCCL) {
+          c->comm = make_nccl_transport(comm->nccl_id, comm->rank, comm->size);
+        } else if (comm->transport == PMG_TRANSPORT_HUB) {
+          need(comm->hub != nullptr && comm->hub->hub.ranks == comm->size, PMG_ERR_CONFIG, "hub / rank count mismatch");
+          c->comm = make_hub_transport(&comm->hub->hub, comm->rank, device);
+          c->use_graphs = false;  // host-mediated exchanges cannot be captured
+        } else {
+          throw PmgError(PMG_ERR_CONFIG, "multi-rank context without a transport");
+        }
+      }
     }
     ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own_stream;
@@ -945,6 +1096,9 @@ int pmg_ctx_create(const pmg_hierarchy_desc* desc, int device, const pmg_comm_de
   } catch (const PmgError& e) {
     g_create_error = e.what();
     return e.code;
+  } catch (const TransportFailure& e) {
+    g_create_error = e.what();
+    return PMG_ERR_TRANSPORT;
   } catch (const std::exception& e) {
     g_create_error = e.what();
     return PMG_ERR_GENERIC;
@@ -954,6 +1108,35 @@ int pmg_ctx_create(const pmg_hierarchy_desc* desc, int device, const pmg_comm_de
 }
 
 void pmg_ctx_destroy(pmg_ctx* ctx) { delete ctx; }
+
+int pmg_nccl_unique_id(unsigned char* out) {
+  const std::string e = nccl_unique_id(out);
+  if (!e.empty()) {
+    g_create_error = e;
+    return PMG_ERR_TRANSPORT;
+  }
+  return PMG_OK;
+}
+
+int pmg_hub_create(int ranks, pmg_hub** out) {
+  if (ranks < 1 || ranks > 64 || !out) {
+    g_create_error = "hub: rank count outside [1, 64]";
+    return PMG_ERR_CONFIG;
+  }
+  *out = new pmg_hub(ranks);
+  return PMG_OK;
+}
+
+void pmg_hub_destroy(pmg_hub* hub) { delete hub; }
+
+int pmg_hub_poison(pmg_hub* hub, const char* reason) {
+  if (hub) hub->hub.poison(reason ? reason : "peer rank failed");
+  return PMG_OK;
+}
+
+int pmg_comm_bytes(pmg_ctx* ctx, uint64_t* out) {
+  return guarded(ctx, [&] { *out = ctx->comm ? ctx->comm->bytes_sent() : 0; });
+}
 
 int pmg_ctx_info(pmg_ctx* ctx, int what, int64_t* out) {
   return guarded(ctx, [&] {

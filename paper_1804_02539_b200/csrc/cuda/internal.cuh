@@ -44,6 +44,13 @@ void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, in
 int fd_rows_per_block();
 int fd_cols_per_block();
 void fd_configure();  // per device, before the first pass
+// whole solve of every piece in one launch, one CTA per piece, tensor and one
+// factor in shared memory: 2 max_total + max_dim^2 doubles <= kFdSmallDoubles
+constexpr long long kFdSmallDoubles = 25000;
+size_t fd_small_smem(long long max_total, int max_dim);
+void launch_fd_small(cudaStream_t s, const FdPiece* pieces, int npieces, int naxes, long long max_total,
+                     int max_dim, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
+                     const double* work_in, double* work_out);
 
 // ---------------------------------------------------------------- SpMV
 struct SpmvArgs {
@@ -87,16 +94,35 @@ struct EdgePiece {
   long long dof_off;  // into the concatenated edge dof list
   const double* Linv; // column-major m x m
 };
-// items: (edge, first row) per CTA, 32 rows each
+// items: (edge, first row) per CTA, 32 rows each.  Piece dofs are interface
+// indices: t holds their totals, rep_off/rep_slot their local replicas.
 void launch_edges_vertices(cudaStream_t s, const EdgePiece* edges, const int2* items, int nitems,
-                           const int* edge_dof_g, const int* vert_g, const double* vert_scalar, int nverts,
-                           const int* rep_off, const int* rep_slot, const double* r, double* out, int add,
+                           const int* edge_iface, const int* vert_iface, const double* vert_scalar, int nverts,
+                           const int* rep_off, const int* rep_slot, const double* t, double* out, int add,
                            double alpha);
+// interface dofs: partial replica sums, exchange packing, ascending-rank fold,
+// write-back to every local replica; piece gathers/scatters through t
+void launch_iface_partial(cudaStream_t s, int n, const int* rep_off, const int* rep_slot, const double* r,
+                          double* tloc);
+void launch_iface_pack(cudaStream_t s, int n, const int* idx, const double* tloc, double* send);
+void launch_iface_combine(cudaStream_t s, int n, const int* comb_off, const int* comb_src, const double* tloc,
+                          const double* recv, double* t);
+void launch_iface_scatter(cudaStream_t s, int n, const int* rep_off, const int* rep_slot, const double* t,
+                          double* out);
+void launch_gather_t(cudaStream_t s, long long n, const int* map, const double* t, double* buf);
+void launch_scatter_iface(cudaStream_t s, long long n, const int* map, const int* rep_off, const int* rep_slot,
+                          const double* buf, double* out, int add, double alpha);
+void launch_sum_ranks(cudaStream_t s, const double* parts, int ranks, int n, double* out);
 // global <-> lattice
 void launch_lattice_from_global(cudaStream_t s, const int* l2g, const unsigned char* owner, long long n, int form,
                                 const double* g, double* lat);
 void launch_global_from_lattice(cudaStream_t s, const int* rep_off, const int* rep_slot, long long ndofs, int form,
                                 const double* lat, double* g);
+// coarse, in steps: rhs[g] = sum of local replicas; x = Ainv rhs; out[slot] = x[l2g]
+void launch_coarse_gather(cudaStream_t s, const int* rep_off, const int* rep_slot, int n0, const double* r,
+                          double* rhs);
+void launch_coarse_gemv(cudaStream_t s, const double* Ainv, int n0, const double* rhs, double* x);
+void launch_coarse_scatter(cudaStream_t s, const int* l2g, long long lat_n, const double* x, double* out);
 // coarse: rhs[g] = sum reps; x = Ainv rhs; out[slot] = x[l2g]
 void launch_coarse(cudaStream_t s, const int* rep_off, const int* rep_slot, const int* l2g, int n0, long long lat_n,
                    const double* Ainv, const double* r, double* rhs, double* x, double* out);
@@ -116,6 +142,11 @@ struct TsDev {
 // output lattice); 2 adds coef * value on non-Dirichlet slots.
 void launch_ts_axis(cudaStream_t s, const TsDev& ts, bool transpose, int K, int d, const int* in_dims, int axis,
                     const double* in, double* out, int mode = 0, const int* l2g = nullptr, double coef = 0.0);
+// single-pass transfers (2D, and 3D levels with small lattices)
+void launch_restrict_fused(cudaStream_t s, const TsDev& ts, int K, int d, int ext_f, int ext_c, const double* r,
+                           double* out, const int* l2g_c);
+void launch_prolong_fused(cudaStream_t s, const TsDev& ts, int K, int d, int ext_f, int ext_c, const double* c,
+                          double coef, double* u, const int* l2g_f);
 // final fine write of a prolongation: u[slot] += c * val where l2g >= 0
 void launch_masked_axpy(cudaStream_t s, const int* l2g, long long n, double c, const double* val, double* u);
 void launch_mask_dirichlet(cudaStream_t s, const int* l2g, long long n, double* v);

@@ -181,9 +181,135 @@ __global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece*
   }
 }
 
+// ---------------------------------------------------------------- small pieces
+// Pieces that fit in shared memory (coarse levels): one CTA runs the whole
+// solve -- gather from the lattice (or a work buffer), d forward products,
+// diagonal division, d backward products, scatter -- with no intermediate
+// global traffic and one launch per smooth instead of 2d.  Same contraction
+// order as FastDiagonalSolver::solve (ascending k per output).
+constexpr int kSmallThreads = 256;
+
+// out(t, j, o) = sum_k B[k*m + j] in(t, k, o) (layout axis 0 fastest) as a
+// GEMM over rows (t, o): each warp owns 8 x 8 output tiles and runs DMMA over
+// k in steps of 4; Bs is B staged in shared memory.
+__device__ void small_axis(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ Bs,
+                           int naxes, const int* dims, int axis) {
+  int inner = 1, outer = 1;
+  for (int a = 0; a < axis; ++a) inner *= dims[a];
+  for (int a = axis + 1; a < naxes; ++a) outer *= dims[a];
+  const int m = dims[axis];
+  const int rows = inner * outer;
+  const int tm_n = (rows + 7) / 8, tn_n = (m + 7) / 8, ks_n = (m + 3) / 4;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  for (int tile = warp; tile < tm_n * tn_n; tile += nwarps) {
+    const int tm = tile % tm_n, tn = tile / tm_n;
+    const int r = tm * 8 + g;  // A row of this lane
+    const bool r_ok = r < rows;
+    const int rt = r_ok ? r % inner : 0, ro = r_ok ? r / inner : 0;
+    const double* arow = in + (long long)ro * inner * m + rt;
+    const int n = tn * 8 + g;  // B column of this lane
+    const bool n_ok = n < m;
+    double d0 = 0.0, d1 = 0.0;
+    for (int ks = 0; ks < ks_n; ++ks) {
+      const int k = ks * 4 + t4;
+      const double a = (r_ok && k < m) ? arow[(long long)k * inner] : 0.0;
+      const double b = (n_ok && k < m) ? Bs[k * m + n] : 0.0;
+      dmma(d0, d1, a, b);
+    }
+    const int orow = tm * 8 + g;
+    if (orow < rows) {
+      const int ot = orow % inner, oo = orow / inner;
+      double* dst = out + (long long)oo * inner * m + ot;
+      const int j0 = tn * 8 + 2 * t4;
+      if (j0 < m) dst[(long long)j0 * inner] = d0;
+      if (j0 + 1 < m) dst[(long long)(j0 + 1) * inner] = d1;
+    }
+  }
+}
+
+__device__ void stage_matrix(double* Bs, const double* __restrict__ B, int m) {
+  for (int i = threadIdx.x; i < m * m; i += blockDim.x) Bs[i] = B[i];
+}
+
+__global__ void __launch_bounds__(kSmallThreads) fd_small_kernel(const FdPiece* __restrict__ pieces, int naxes,
+                                                                 int in_mode, int out_mode,
+                                                                 const double* __restrict__ lat_in,
+                                                                 double* __restrict__ lat_out, double alpha,
+                                                                 const double* __restrict__ work_in,
+                                                                 double* __restrict__ work_out) {
+  extern __shared__ double sm[];
+  const FdPiece& P = pieces[blockIdx.x];
+  const int dims[3] = {P.dims[0], P.dims[1], naxes == 3 ? P.dims[2] : 1};
+  const int total = int(P.total);
+  double* X = sm;
+  double* Y = sm + total;
+  double* Bs = sm + 2 * total;
+  const long long ext = P.ext, ext2 = (long long)P.ext * P.ext;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    double v;
+    if (in_mode == FD_IN_WORK) {
+      v = work_in[P.work_off + idx];
+    } else {
+      const int i0 = idx % dims[0], i1 = (idx / dims[0]) % dims[1], i2 = idx / (dims[0] * dims[1]);
+      v = lat_in[P.lat_base + i0 + ext * i1 + ext2 * i2];
+    }
+    X[idx] = v;
+  }
+  __syncthreads();
+  for (int a = 0; a < naxes; ++a) {  // w = (x_a V_a^T) r
+    stage_matrix(Bs, P.B[a][0], dims[a]);
+    __syncthreads();
+    small_axis(X, Y, Bs, naxes, dims, a);
+    __syncthreads();
+    double* tmp = X;
+    X = Y;
+    Y = tmp;
+  }
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) X[idx] = X[idx] / P.diag[idx];
+  __syncthreads();
+  for (int a = 0; a < naxes; ++a) {  // x = (x_a V_a) w
+    stage_matrix(Bs, P.B[a][1], dims[a]);
+    __syncthreads();
+    small_axis(X, Y, Bs, naxes, dims, a);
+    __syncthreads();
+    double* tmp = X;
+    X = Y;
+    Y = tmp;
+  }
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const double v = X[idx];
+    if (out_mode == FD_OUT_WORK || out_mode == FD_OUT_WORK_DIAG) {
+      work_out[P.work_off + idx] = v;
+    } else {
+      const int i0 = idx % dims[0], i1 = (idx / dims[0]) % dims[1], i2 = idx / (dims[0] * dims[1]);
+      const long long lat = P.lat_base + i0 + ext * i1 + ext2 * i2;
+      if (out_mode == FD_OUT_LATTICE_SET)
+        lat_out[lat] = alpha * v;
+      else
+        lat_out[lat] += alpha * v;
+    }
+  }
+}
+
 }  // namespace
 
-void fd_configure() {}
+size_t fd_small_smem(long long max_total, int max_dim) {
+  return size_t(2 * max_total + (long long)max_dim * max_dim) * sizeof(double);
+}
+
+void launch_fd_small(cudaStream_t s, const FdPiece* pieces, int npieces, int naxes, long long max_total,
+                     int max_dim, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
+                     const double* work_in, double* work_out) {
+  if (npieces == 0) return;
+  const size_t smem = fd_small_smem(max_total, max_dim);
+  fd_small_kernel<<<npieces, kSmallThreads, smem, s>>>(pieces, naxes, in_mode, out_mode, lat_in, lat_out, alpha,
+                                                       work_in, work_out);
+}
+
+void fd_configure() {
+  cudaFuncSetAttribute(fd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
 
 int fd_rows_per_block() { return kBM; }
 int fd_cols_per_block() { return kBN; }

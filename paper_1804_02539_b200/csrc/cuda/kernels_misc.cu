@@ -118,21 +118,18 @@ __global__ void scatter_kernel(const int* __restrict__ dof_g, long long ndof, co
 // vertex piece (smoother.cpp:36-38).
 __global__ void __launch_bounds__(kThreads) edges_vertices_kernel(
     const EdgePiece* __restrict__ edges, const int2* __restrict__ items, int nitems,
-    const int* __restrict__ edge_dof_g, const int* __restrict__ vert_g, const double* __restrict__ vert_scalar,
-    int nverts, const int* __restrict__ rep_off, const int* __restrict__ rep_slot, const double* __restrict__ r,
+    const int* __restrict__ edge_iface, const int* __restrict__ vert_iface, const double* __restrict__ vert_scalar,
+    int nverts, const int* __restrict__ rep_off, const int* __restrict__ rep_slot, const double* __restrict__ t,
     double* __restrict__ out, int add, double alpha) {
+  // t: interface totals (sum over every replica, all ranks); rep_off/rep_slot:
+  // this rank's replicas of each interface dof
   __shared__ double buf[512];
   __shared__ double part[kThreads / 32][32];
   if (blockIdx.x < nitems) {
     const int2 it = items[blockIdx.x];
     const EdgePiece e = edges[it.x];
-    const int* dofs = edge_dof_g + e.dof_off;
-    for (int i = threadIdx.x; i < e.m; i += kThreads) {
-      const int g = dofs[i];
-      double s = 0.0;
-      for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) s += r[rep_slot[q]];
-      buf[i] = s;
-    }
+    const int* dofs = edge_iface + e.dof_off;
+    for (int i = threadIdx.x; i < e.m; i += kThreads) buf[i] = t[dofs[i]];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i = it.y + lane;
@@ -163,10 +160,8 @@ __global__ void __launch_bounds__(kThreads) edges_vertices_kernel(
     return;
   }
   for (int v = threadIdx.x; v < nverts; v += kThreads) {
-    const int g = vert_g[v];
-    double s = 0.0;
-    for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) s += r[rep_slot[q]];
-    const double z = s / vert_scalar[v];
+    const int g = vert_iface[v];
+    const double z = t[g] / vert_scalar[v];
     for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) {
       if (add)
         out[rep_slot[q]] += alpha * z;
@@ -192,8 +187,8 @@ __global__ void global_from_lattice_kernel(const int* __restrict__ rep_off, cons
                                            double* __restrict__ g) {
   const long long d = blockIdx.x * (long long)kThreads + threadIdx.x;
   if (d >= ndofs) return;
-  if (form == 0) {
-    g[d] = lat[rep_slot[rep_off[d]]];
+  if (form == 0) {  // dofs without a replica on this rank read as 0
+    g[d] = rep_off[d] < rep_off[d + 1] ? lat[rep_slot[rep_off[d]]] : 0.0;
   } else {
     double s = 0.0;
     for (int q = rep_off[d]; q < rep_off[d + 1]; ++q) s += lat[rep_slot[q]];
@@ -270,6 +265,149 @@ __global__ void ts_axis_kernel(TsDev ts, int transpose, int K, int d, int in0, i
       out[idx] = l2g[idx] >= 0 ? s : 0.0;
     else if (l2g[idx] >= 0)
       out[idx] += coef * s;
+  }
+}
+
+// ---------------------------------------------------------------- interface sums
+// T_loc[i] = sum of this rank's replicas of interface dof i (ascending slot)
+__global__ void iface_partial_kernel(int n, const int* __restrict__ rep_off, const int* __restrict__ rep_slot,
+                                     const double* __restrict__ r, double* __restrict__ tloc) {
+  const int i = blockIdx.x * kThreads + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int q = rep_off[i]; q < rep_off[i + 1]; ++q) s += r[rep_slot[q]];
+  tloc[i] = s;
+}
+
+__global__ void iface_pack_kernel(int n, const int* __restrict__ idx, const double* __restrict__ tloc,
+                                  double* __restrict__ send) {
+  const int q = blockIdx.x * kThreads + threadIdx.x;
+  if (q < n) send[q] = tloc[idx[q]];
+}
+
+// ascending-rank fold of the partials (ParallelBackend::accumulate order)
+__global__ void iface_combine_kernel(int n, const int* __restrict__ comb_off, const int* __restrict__ comb_src,
+                                     const double* __restrict__ tloc, const double* __restrict__ recv,
+                                     double* __restrict__ t) {
+  const int i = blockIdx.x * kThreads + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int q = comb_off[i]; q < comb_off[i + 1]; ++q) {
+    const int src = comb_src[q];
+    s += src < 0 ? tloc[i] : recv[src];
+  }
+  t[i] = s;
+}
+
+__global__ void iface_scatter_kernel(int n, const int* __restrict__ rep_off, const int* __restrict__ rep_slot,
+                                     const double* __restrict__ t, double* __restrict__ out) {
+  const int i = blockIdx.x * kThreads + threadIdx.x;
+  if (i >= n) return;
+  const double v = t[i];
+  for (int q = rep_off[i]; q < rep_off[i + 1]; ++q) out[rep_slot[q]] = v;
+}
+
+__global__ void gather_t_kernel(long long n, const int* __restrict__ map, const double* __restrict__ t,
+                                double* __restrict__ buf) {
+  const long long j = blockIdx.x * (long long)kThreads + threadIdx.x;
+  if (j < n) buf[j] = t[map[j]];
+}
+
+__global__ void scatter_iface_kernel(long long n, const int* __restrict__ map, const int* __restrict__ rep_off,
+                                     const int* __restrict__ rep_slot, const double* __restrict__ buf,
+                                     double* __restrict__ out, int add, double alpha) {
+  const long long j = blockIdx.x * (long long)kThreads + threadIdx.x;
+  if (j >= n) return;
+  const int i = map[j];
+  const double v = buf[j];
+  for (int q = rep_off[i]; q < rep_off[i + 1]; ++q) {
+    if (add)
+      out[rep_slot[q]] += alpha * v;
+    else
+      out[rep_slot[q]] = alpha * v;
+  }
+}
+
+// ascending-rank sums: out[d] = sum_r parts[r * n + d]
+__global__ void sum_ranks_kernel(const double* __restrict__ parts, int ranks, int n, double* __restrict__ out) {
+  const int d = blockIdx.x * kThreads + threadIdx.x;
+  if (d >= n) return;
+  double s = 0.0;
+  for (int r = 0; r < ranks; ++r) s += parts[(long long)r * n + d];
+  out[d] = s;
+}
+
+// Whole tensor transfer in one pass, one output per thread; the nested sums run
+// axis 0 innermost, i.e. in the order of the reference's successive
+// apply_along_axis calls (restrict_patch / prolong_patch, transfer.cpp:21-66).
+// Restriction (transpose): coarse(j) = sum_i2 P(i2,j2) sum_i1 P(i1,j1) sum_i0 P(i0,j0) r(i)
+// with Dirichlet coarse slots zeroed; prolongation: u(i) += coef * sum over
+// the <= p+1 parents per axis, on non-Dirichlet fine slots.
+__global__ void restrict_fused_kernel(TsDev ts, int K, int d, int ext_f, int ext_c, const double* __restrict__ r,
+                                      double* __restrict__ out, const int* __restrict__ l2g_c) {
+  long long Sc = 1, Sf = 1;
+  for (int a = 0; a < d; ++a) {
+    Sc *= ext_c;
+    Sf *= ext_f;
+  }
+  const long long total = Sc * K;
+  for (long long idx = blockIdx.x * (long long)kThreads + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * kThreads) {
+    if (l2g_c[idx] < 0) {
+      out[idx] = 0.0;
+      continue;
+    }
+    const long long k = idx / Sc;
+    const long long rem = idx - k * Sc;
+    const int j0 = int(rem % ext_c), j1 = int((rem / ext_c) % ext_c), j2 = d == 3 ? int(rem / ((long long)ext_c * ext_c)) : 0;
+    const double* src = r + k * Sf;
+    double s2 = 0.0;
+    const int q2a = d == 3 ? ts.col_off[j2] : 0, q2b = d == 3 ? ts.col_off[j2 + 1] : 1;
+    for (int q2 = q2a; q2 < q2b; ++q2) {
+      const long long b2 = d == 3 ? (long long)ts.col_row[q2] * ext_f * ext_f : 0;
+      double s1 = 0.0;
+      for (int q1 = ts.col_off[j1]; q1 < ts.col_off[j1 + 1]; ++q1) {
+        const double* row = src + b2 + (long long)ts.col_row[q1] * ext_f;
+        double s0 = 0.0;
+        for (int q0 = ts.col_off[j0]; q0 < ts.col_off[j0 + 1]; ++q0) s0 = fma(ts.col_val[q0], row[ts.col_row[q0]], s0);
+        s1 = fma(ts.col_val[q1], s0, s1);
+      }
+      s2 = d == 3 ? fma(ts.col_val[q2], s1, s2) : s1;
+    }
+    out[idx] = s2;
+  }
+}
+
+__global__ void prolong_fused_kernel(TsDev ts, int K, int d, int ext_f, int ext_c, const double* __restrict__ c,
+                                     double coef, double* __restrict__ u, const int* __restrict__ l2g_f) {
+  long long Sc = 1, Sf = 1;
+  for (int a = 0; a < d; ++a) {
+    Sc *= ext_c;
+    Sf *= ext_f;
+  }
+  const long long total = Sf * K;
+  for (long long idx = blockIdx.x * (long long)kThreads + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * kThreads) {
+    if (l2g_f[idx] < 0) continue;
+    const long long k = idx / Sf;
+    const long long rem = idx - k * Sf;
+    const int i0 = int(rem % ext_f), i1 = int((rem / ext_f) % ext_f), i2 = d == 3 ? int(rem / ((long long)ext_f * ext_f)) : 0;
+    const double* src = c + k * Sc;
+    const int n2 = d == 3 ? ts.row_len[i2] : 1;
+    double s2 = 0.0;
+    for (int q2 = 0; q2 < n2; ++q2) {
+      const long long b2 = d == 3 ? (long long)(ts.row_start[i2] + q2) * ext_c * ext_c : 0;
+      double s1 = 0.0;
+      for (int q1 = 0; q1 < ts.row_len[i1]; ++q1) {
+        const double* row = src + b2 + (long long)(ts.row_start[i1] + q1) * ext_c + ts.row_start[i0];
+        const double* v0 = ts.vals + ts.row_off[i0];
+        double s0 = 0.0;
+        for (int q0 = 0; q0 < ts.row_len[i0]; ++q0) s0 = fma(v0[q0], row[q0], s0);
+        s1 = fma(ts.vals[ts.row_off[i1] + q1], s0, s1);
+      }
+      s2 = d == 3 ? fma(ts.vals[ts.row_off[i2] + q2], s1, s2) : s1;
+    }
+    u[idx] += coef * s2;
   }
 }
 
@@ -398,6 +536,16 @@ void launch_coarse(cudaStream_t s, const int* rep_off, const int* rep_slot, cons
   }
   coarse_scatter_kernel<<<grid_for(lat_n), kThreads, 0, s>>>(l2g, lat_n, x, out);
 }
+void launch_coarse_gather(cudaStream_t s, const int* rep_off, const int* rep_slot, int n0, const double* r,
+                          double* rhs) {
+  if (n0 > 0) coarse_gather_kernel<<<grid_for(n0), kThreads, 0, s>>>(rep_off, rep_slot, n0, r, rhs);
+}
+void launch_coarse_gemv(cudaStream_t s, const double* Ainv, int n0, const double* rhs, double* x) {
+  if (n0 > 0) coarse_gemv_kernel<<<grid_for((long long)n0 * 32), kThreads, 0, s>>>(Ainv, n0, rhs, x);
+}
+void launch_coarse_scatter(cudaStream_t s, const int* l2g, long long lat_n, const double* x, double* out) {
+  coarse_scatter_kernel<<<grid_for(lat_n), kThreads, 0, s>>>(l2g, lat_n, x, out);
+}
 void launch_ts_axis(cudaStream_t s, const TsDev& ts, bool transpose, int K, int d, const int* in_dims, int axis,
                     const double* in, double* out, int mode, const int* l2g, double coef) {
   long long per_out = 1;
@@ -407,6 +555,44 @@ void launch_ts_axis(cudaStream_t s, const TsDev& ts, bool transpose, int K, int 
   if (g > 148LL * 32) g = 148LL * 32;
   ts_axis_kernel<<<int(g < 1 ? 1 : g), kThreads, 0, s>>>(ts, transpose ? 1 : 0, K, d, in_dims[0], in_dims[1],
                                                          d == 3 ? in_dims[2] : 1, axis, in, out, mode, l2g, coef);
+}
+void launch_iface_partial(cudaStream_t s, int n, const int* rep_off, const int* rep_slot, const double* r,
+                          double* tloc) {
+  if (n > 0) iface_partial_kernel<<<grid_for(n), kThreads, 0, s>>>(n, rep_off, rep_slot, r, tloc);
+}
+void launch_iface_pack(cudaStream_t s, int n, const int* idx, const double* tloc, double* send) {
+  if (n > 0) iface_pack_kernel<<<grid_for(n), kThreads, 0, s>>>(n, idx, tloc, send);
+}
+void launch_iface_combine(cudaStream_t s, int n, const int* comb_off, const int* comb_src, const double* tloc,
+                          const double* recv, double* t) {
+  if (n > 0) iface_combine_kernel<<<grid_for(n), kThreads, 0, s>>>(n, comb_off, comb_src, tloc, recv, t);
+}
+void launch_iface_scatter(cudaStream_t s, int n, const int* rep_off, const int* rep_slot, const double* t,
+                          double* out) {
+  if (n > 0) iface_scatter_kernel<<<grid_for(n), kThreads, 0, s>>>(n, rep_off, rep_slot, t, out);
+}
+void launch_gather_t(cudaStream_t s, long long n, const int* map, const double* t, double* buf) {
+  if (n > 0) gather_t_kernel<<<grid_for(n), kThreads, 0, s>>>(n, map, t, buf);
+}
+void launch_scatter_iface(cudaStream_t s, long long n, const int* map, const int* rep_off, const int* rep_slot,
+                          const double* buf, double* out, int add, double alpha) {
+  if (n > 0)
+    scatter_iface_kernel<<<grid_for(n), kThreads, 0, s>>>(n, map, rep_off, rep_slot, buf, out, add, alpha);
+}
+void launch_sum_ranks(cudaStream_t s, const double* parts, int ranks, int n, double* out) {
+  if (n > 0) sum_ranks_kernel<<<grid_for(n), kThreads, 0, s>>>(parts, ranks, n, out);
+}
+void launch_restrict_fused(cudaStream_t s, const TsDev& ts, int K, int d, int ext_f, int ext_c, const double* r,
+                           double* out, const int* l2g_c) {
+  long long n = K;
+  for (int a = 0; a < d; ++a) n *= ext_c;
+  restrict_fused_kernel<<<grid_for(n), kThreads, 0, s>>>(ts, K, d, ext_f, ext_c, r, out, l2g_c);
+}
+void launch_prolong_fused(cudaStream_t s, const TsDev& ts, int K, int d, int ext_f, int ext_c, const double* c,
+                          double coef, double* u, const int* l2g_f) {
+  long long n = K;
+  for (int a = 0; a < d; ++a) n *= ext_f;
+  prolong_fused_kernel<<<grid_for(n), kThreads, 0, s>>>(ts, K, d, ext_f, ext_c, c, coef, u, l2g_f);
 }
 void launch_masked_axpy(cudaStream_t s, const int* l2g, long long n, double c, const double* val, double* u) {
   if (n > 0) masked_axpy_kernel<<<grid_for(n), kThreads, 0, s>>>(l2g, n, c, val, u);

@@ -1,0 +1,81 @@
+"""The multi-rank data path on one GPU: R contexts, each owning a contiguous
+patch block, exchange interface sums, scalar reductions and the coarse
+residual through the in-process hub (host-mediated device copies; no kernel
+waits on another rank).  The same plans, packing and ordered folds run over
+NCCL under torchrun.  Mirrors test_parallel.cpp:278-625."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1804_02539_b200 import Hierarchy
+from paper_1804_02539_b200.parallel import local_dof_mask, parallel_pcg_solve, run_ranks
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("c2", 4, 3, 2, "default"), ("fichera", 2, 2, 1, "sine3d"), ("c5", 3, 2, 2, "default"),
+         ("c4", 3, 2, 2, "default")]
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])
+def hier(request):
+    dom, p, lv, n0, rhs = request.param
+    h = Hierarchy(dom, p, lv, n0=n0, rhs=rhs)
+    return h, oracle.Oracle(h)
+
+
+def rand(n, seed):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_operations_match_serial(hier, R):  # test_parallel.cpp:278-524
+    h, o = hier
+    L = h.finest_level
+    g = rand(h.num_dofs(L), 7)
+    u = rand(h.num_dofs(L), 8)
+    g0 = rand(h.num_dofs(0), 9)
+    ref_smooth = o.smooth(L, g)
+    ref_coarse = o.coarse_solve(g0)
+    ref_au = o.apply_op(L, u)
+
+    def body(r, b):
+        acc = b.gather_global(L, b.accumulate(L, b.to_distributed_owner(L, g)))
+        sm = b.gather_global(L, b.smooth(L, b.to_distributed_owner(L, g)))
+        au = b.apply_op(L, b.to_accumulated(L, u))
+        au_loc = b.gather_global(L, au)
+        cs = b.gather_global(0, b.coarse_solve(b.to_distributed_owner(0, g0)))
+        dt = b.dot(L, b.to_distributed_owner(L, g), b.to_accumulated(L, u))
+        return acc, sm, au_loc, cs, dt
+
+    out = run_ranks(h, R, body)
+    for r, (acc, sm, au_loc, cs, dt) in enumerate(out):
+        m = local_dof_mask(h, L, r, R)
+        m0 = local_dof_mask(h, 0, r, R)
+        # accumulate reassembles the owner split exactly (test_parallel.cpp:278-376)
+        assert np.array_equal(acc[m], g[m])
+        assert np.abs(sm[m] - ref_smooth[m]).max() <= 1e-12 * np.abs(ref_smooth).max()
+        assert np.abs(cs[m0] - ref_coarse[m0]).max() <= 1e-12 * np.abs(ref_coarse).max()
+        assert dt == out[0][4]  # every rank holds the same reduced bits
+        assert abs(dt - g @ u) <= 1e-13 * np.abs(g * u).sum()
+    # apply_op shares sum to the serial operator
+    total = sum(o_[2] for o_ in out)
+    assert np.abs(total - ref_au).max() <= 1e-13 * (1 + np.abs(ref_au).max())
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_parallel_solve_tracks_serial(hier, R):  # test_parallel.cpp:581-625
+    h, o = hier
+    f = h.rhs()
+    u_ser, hist_ser, _, _ = o.pcg_solve(f)
+    u_par, hist_par, _, _ = o.pcg_solve(f, ranks=R)
+    u, rep, nbytes = parallel_pcg_solve(h, R, f)
+    assert nbytes > 0
+    assert rep.iterations == len(hist_ser) - 1 == len(hist_par) - 1
+    scale = np.abs(u_ser).max()
+    assert np.abs(u - u_ser).max() <= 1e-10 * scale
+    hist = np.array(rep.residual_history)
+    k = min(5, len(hist))
+    assert np.all(np.abs(hist[:k] - hist_ser[:k]) <= 1e-10 * hist_ser[:k])
+    # same partition, same exchange order: a rerun reproduces every bit
+    _, rep2, _ = parallel_pcg_solve(h, R, f)
+    assert rep2.residual_history == rep.residual_history
