@@ -55,6 +55,24 @@ int pmgh_reps(pmgh_hierarchy* h, int level, const int32_t** off, const int32_t**
  * (patch_a, side_a, patch_b, side_b, orientation). */
 int pmgh_interfaces(pmgh_hierarchy* h, int* count, const int32_t** data);
 
+/* Interface-dof exchange plan of `rank` among `ranks` on `level` -- the plan
+ * libpmg_cuda builds internally (csrc/common/rank_plan.hpp), exposed so the
+ * CPU tests can run the exchange protocol over torch.distributed/gloo.
+ * Arrays stay valid until the next call on h. */
+typedef struct {
+  int n_iface;
+  const int32_t* iface_g;   /* [n_iface] global ids, ascending */
+  const int32_t* rep_off;   /* [n_iface+1] local replicas (rank-local lattice slots) */
+  const int32_t* rep_slot;
+  const int32_t* comb_off;  /* [n_iface+1] fold sources, ascending rank */
+  const int32_t* comb_src;  /* -1 = own partial, else index into the concatenated receive buffers */
+  int n_neighbors;
+  const int32_t* nb_rank;   /* [n_neighbors] ascending */
+  const int32_t* nb_off;    /* [n_neighbors+1] into nb_iface */
+  const int32_t* nb_iface;  /* interface positions exchanged with each neighbour, ascending */
+} pmgh_rank_plan_view;
+int pmgh_rank_plan(pmgh_hierarchy* h, int level, int ranks, int rank, pmgh_rank_plan_view* out);
+
 /* ---- numerics hooks used by the known-answer tests ---- */
 int pmgh_gauss_legendre(int points, double* nodes, double* weights);
 /* first_index and values[degree+1] */

@@ -52,6 +52,13 @@ class PmgCommDesc(C.Structure):
 
 PMG_TRANSPORT_NONE, PMG_TRANSPORT_NCCL, PMG_TRANSPORT_HUB = 0, 1, 2
 
+
+class PmghRankPlanView(C.Structure):
+    _fields_ = [("n_iface", C.c_int), ("iface_g", C.POINTER(C.c_int32)), ("rep_off", C.POINTER(C.c_int32)),
+                ("rep_slot", C.POINTER(C.c_int32)), ("comb_off", C.POINTER(C.c_int32)),
+                ("comb_src", C.POINTER(C.c_int32)), ("n_neighbors", C.c_int), ("nb_rank", C.POINTER(C.c_int32)),
+                ("nb_off", C.POINTER(C.c_int32)), ("nb_iface", C.POINTER(C.c_int32))]
+
 PMG_OK = 0
 PMG_ERR_CONFIG = 2
 PMG_ERR_DIVERGENCE = 3
@@ -99,6 +106,7 @@ def host_lib():
         _sig(lib, "pmgh_stored_entries", C.c_int64, [C.c_int, C.c_int, C.c_int, C.c_int])
         _sig(lib, "pmgh_reps", C.c_int, [_vp, C.c_int, C.POINTER(_ip), C.POINTER(_ip), C.POINTER(_ip)])
         _sig(lib, "pmgh_interfaces", C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(_ip)])
+        _sig(lib, "pmgh_rank_plan", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(PmghRankPlanView)])
         _sig(lib, "pmgh_gauss_legendre", C.c_int, [C.c_int, _dp, _dp])
         _sig(lib, "pmgh_eval_basis", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                                C.POINTER(C.c_int), _dp])

@@ -71,10 +71,22 @@ def build_cuda(force: bool = False) -> Path:
     return out
 
 
+def build_example(force: bool = False) -> Path:
+    """C++ driver of include/patchmg_gpu.hpp (the Backend-concept mirror)."""
+    host, cuda = build_host(force), build_cuda(force)
+    src = PKG / "csrc" / "examples" / "pcg_cpp.cpp"
+    out = LIB / "pcg_cpp"
+    if force or _stale(out, [src, host, cuda]):
+        _run(["g++", "-O2", "-std=c++17", "-I" + str(ROOT / "include"), "-o", out, src, "-L" + str(LIB),
+              "-lpmg_cuda", "-lpmg_host", "-Wl,-rpath,$ORIGIN", "-pthread"])
+    return out
+
+
 def build_all(force: bool = False) -> None:
     build_host(force)
     build_oracle(force)
     build_cuda(force)
+    build_example(force)
 
 
 if __name__ == "__main__":

@@ -5,6 +5,7 @@
 #include <string>
 
 #include "../../../include/pmg_host.h"
+#include "../common/rank_plan.hpp"
 #include "hierarchy.hpp"
 
 using namespace pmg;
@@ -18,6 +19,8 @@ struct pmgh_hierarchy {
   std::vector<std::vector<double>> ts_vals;
   std::vector<std::int32_t> interfaces;
   std::vector<double> rhs;
+  pmgplan::RankPlan plan;  // last pmgh_rank_plan result
+  std::vector<std::int32_t> nb_rank, nb_off, nb_iface;
 };
 
 namespace {
@@ -263,6 +266,40 @@ int pmgh_interfaces(pmgh_hierarchy* H, int* count, const int32_t** data) {
   *count = int(H->interfaces.size() / 5);
   *data = H->interfaces.data();
   return PMG_OK;
+}
+
+int pmgh_rank_plan(pmgh_hierarchy* H, int level, int ranks, int rank, pmgh_rank_plan_view* out) {
+  if (!H || !out || level < 0 || level >= H->h->num_levels()) return fail(PMG_ERR_CONFIG, "pmgh_rank_plan: bad args");
+  return guarded([&] {
+    const Level& L = H->h->level(level);
+    pmgplan::Partition part;
+    try {
+      part = pmgplan::contiguous(H->h->num_patches(), ranks);
+    } catch (const std::invalid_argument& e) {
+      throw ConfigError(e.what());
+    }
+    if (rank < 0 || rank >= ranks) throw ConfigError("pmgh_rank_plan: rank out of range");
+    H->plan = pmgplan::build(L.l2g.data(), H->h->num_patches(), L.mapper->lattice_size(), L.mapper->num_dofs(), part,
+                             rank);
+    H->nb_rank.clear();
+    H->nb_off.assign(1, 0);
+    H->nb_iface.clear();
+    for (const auto& nb : H->plan.neighbors) {
+      H->nb_rank.push_back(nb.rank);
+      H->nb_iface.insert(H->nb_iface.end(), nb.iface.begin(), nb.iface.end());
+      H->nb_off.push_back(int(H->nb_iface.size()));
+    }
+    out->n_iface = int(H->plan.iface_g.size());
+    out->iface_g = H->plan.iface_g.data();
+    out->rep_off = H->plan.rep_off.data();
+    out->rep_slot = H->plan.rep_slot.data();
+    out->comb_off = H->plan.comb_off.data();
+    out->comb_src = H->plan.comb_src.data();
+    out->n_neighbors = int(H->nb_rank.size());
+    out->nb_rank = H->nb_rank.data();
+    out->nb_off = H->nb_off.data();
+    out->nb_iface = H->nb_iface.data();
+  });
 }
 
 int pmgh_gauss_legendre(int points, double* nodes, double* weights) {
