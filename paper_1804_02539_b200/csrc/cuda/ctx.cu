@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -44,6 +45,7 @@ void ck(cudaError_t e, const char* what) {
 
 struct DevLevel {
   int n = 0, ext = 0, O = 0, K = 0;
+  int Ob = 0;  // stored offsets per patch: O, or (O+1)/2 for the symmetric half band
   long long S = 0, Sp = 0, lat_n = 0, N = 0;
   double* band = nullptr;
   int* l2g = nullptr;
@@ -55,6 +57,7 @@ struct DevLevel {
   int n_iface = 0;
   int *if_rep_off = nullptr, *if_rep_slot = nullptr, *if_comb_off = nullptr, *if_comb_src = nullptr;
   double *if_tloc = nullptr, *if_t = nullptr;
+  const double* if_total = nullptr;  // the totals: if_t, or if_tloc itself on one rank
   int* if_send_idx = nullptr;
   int n_send = 0, n_recv = 0;
   double *if_send = nullptr, *if_recv = nullptr;
@@ -192,7 +195,8 @@ struct pmg_ctx {
   T* alloc(size_t count) {
     void* p = nullptr;
     if (count == 0) count = 1;
-    ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    // 64 B of slack: TMA windows over a lattice vector round its end up to 16 B
+    ck(cudaMalloc(&p, count * sizeof(T) + 64), "cudaMalloc");
     allocs.push_back(p);
     bytes += count * sizeof(T);
     return static_cast<T*>(p);
@@ -200,7 +204,7 @@ struct pmg_ctx {
   template <class T>
   T* upload(const T* h, size_t count) {
     T* d = alloc<T>(count);
-    if (count) ck(cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    if (count) ck(cudaMemcpyAsync(d, h, count * sizeof(T), cudaMemcpyHostToDevice, stream), "cudaMemcpy H2D");
     return d;
   }
   template <class T>
@@ -296,14 +300,22 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   const int* l2g_all = ld.l2g;
   const int* l2g = l2g_all + (size_t)c.pb * S;
 
-  // ---- band: rows of one (patch, offset) pair at stride Sp (>= S, see spmv_padded_rows)
-  L.Sp = spmv_padded_rows(d, p, S);
+  // ---- band: rows of one (patch, offset) pair at stride Sp (>= S, see spmv_row_stride)
+  L.Sp = spmv_row_stride(d, p, L.ext, S);
   const long long Sp = L.Sp;
-  L.band = c.alloc<double>(size_t(L.K) * L.O * Sp);
+  // the symmetric half band (kernels_spmv.cu) on TMA levels; PMG_FULL_BAND=1 keeps all O offsets
+  const char* fb = std::getenv("PMG_FULL_BAND");
+  L.Ob = spmv_stored_offsets(d, p, S, !(fb && fb[0] == '1'));
+  // slack past the last patch: mirrored segments read up to Sp + 2 rows beyond a patch's rows
+  const size_t band_n = size_t(L.K) * L.Ob * Sp + size_t(Sp) + 256;
+  L.band = c.alloc<double>(band_n);
+  ck(cudaMemsetAsync(L.band, 0, band_n * sizeof(double), c.stream), "band clear");
   if (ld.band_format == PMG_BAND_TENSOR) {
-    ck(cudaMemcpy2D(L.band, sizeof(double) * Sp, ld.band + (size_t)c.pb * L.O * S, sizeof(double) * S,
-                    sizeof(double) * S, size_t(L.K) * L.O, cudaMemcpyHostToDevice),
-       "band upload");
+    for (int k = 0; k < L.K; ++k)
+      ck(cudaMemcpy2DAsync(L.band + size_t(k) * L.Ob * Sp, sizeof(double) * Sp,
+                           ld.band + (size_t)(c.pb + k) * L.O * S, sizeof(double) * S, sizeof(double) * S,
+                           size_t(L.Ob), cudaMemcpyHostToDevice, c.stream),
+         "band upload");
   } else if (ld.band_format == PMG_BAND_CSR) {
     // place every CSR entry at its tensor offset (PatchOperator, assembly.hpp:16-25)
     std::vector<double> hb(size_t(L.O) * S);
@@ -327,15 +339,16 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
           }
           hb[size_t(o) * S + r] += vals[q];
         }
-      ck(cudaMemcpy2D(L.band + size_t(k) * L.O * Sp, sizeof(double) * Sp, hb.data(), sizeof(double) * S,
-                      sizeof(double) * S, size_t(L.O), cudaMemcpyHostToDevice),
+      // pageable source: the call returns once hb is staged, so hb is reusable
+      ck(cudaMemcpy2DAsync(L.band + size_t(k) * L.Ob * Sp, sizeof(double) * Sp, hb.data(), sizeof(double) * S,
+                           sizeof(double) * S, size_t(L.Ob), cudaMemcpyHostToDevice, c.stream),
          "band upload");
     }
   } else {
     throw PmgError(PMG_ERR_CONFIG, "unknown band format");
   }
   L.l2g = c.upload(l2g, size_t(L.lat_n));
-  launch_zero_dirichlet_band(c.stream, d, p, L.ext, S, Sp, L.K, L.l2g, L.band);
+  launch_zero_dirichlet_band(c.stream, d, p, L.ext, S, Sp, L.K, L.Ob, L.l2g, L.band);
 
   // ---- replicas: global owner patch over all patches; local replica CSR
   std::vector<int> owner_patch(size_t(L.N), -1);
@@ -369,6 +382,7 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   L.if_comb_src = c.upload(plan.comb_src);
   L.if_tloc = c.alloc<double>(size_t(L.n_iface));
   L.if_t = c.alloc<double>(size_t(L.n_iface));
+  L.if_total = c.size > 1 ? L.if_t : L.if_tloc;
   std::vector<int> send_idx;
   for (const auto& nb : plan.neighbors) send_idx.insert(send_idx.end(), nb.iface.begin(), nb.iface.end());
   L.n_send = L.n_recv = int(send_idx.size());
@@ -519,8 +533,14 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   for (const auto& fp : h_face) L.face_max_total = std::max(L.face_max_total, fp.total);
   L.int_max_dim = maxdim_int;
   L.face_max_dim = maxdim_face;
-  L.int_small = 2 * L.int_max_total + (long long)maxdim_int * maxdim_int <= kFdSmallDoubles;
-  L.face_small = 2 * L.face_max_total + (long long)maxdim_face * maxdim_face <= kFdSmallDoubles;
+  // one CTA per piece only while the piece is small enough that the pass
+  // kernels (many CTAs per piece) would not be faster
+  const char* fsm = std::getenv("PMG_FD_SMALL_MAX");
+  const long long small_max = fsm ? std::atoll(fsm) : 2048;
+  L.int_small = 2 * L.int_max_total + (long long)maxdim_int * maxdim_int <= kFdSmallDoubles &&
+                L.int_max_total <= small_max;
+  L.face_small = 2 * L.face_max_total + (long long)maxdim_face * maxdim_face <= kFdSmallDoubles &&
+                 L.face_max_total <= small_max;
   L.n_int = int(h_int.size());
   L.d_int = c.upload(h_int);
   L.n_face = int(h_face.size());
@@ -590,9 +610,9 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   L.f = c.alloc<double>(size_t(L.lat_n));
   L.u = c.alloc<double>(size_t(L.lat_n));
   L.r = c.alloc<double>(size_t(L.lat_n));
-  ck(cudaMemset(L.f, 0, sizeof(double) * L.lat_n), "memset");
-  ck(cudaMemset(L.u, 0, sizeof(double) * L.lat_n), "memset");
-  ck(cudaMemset(L.r, 0, sizeof(double) * L.lat_n), "memset");
+  ck(cudaMemsetAsync(L.f, 0, sizeof(double) * L.lat_n, c.stream), "memset");
+  ck(cudaMemsetAsync(L.u, 0, sizeof(double) * L.lat_n, c.stream), "memset");
+  ck(cudaMemsetAsync(L.r, 0, sizeof(double) * L.lat_n, c.stream), "memset");
 }
 
 void build_ctx(pmg_ctx& c, const pmg_hierarchy_desc& D) {
@@ -645,14 +665,14 @@ void build_ctx(pmg_ctx& c, const pmg_hierarchy_desc& D) {
   for (auto& L : c.lv) c.partial_n = std::max(c.partial_n, spmv_partials(c.dim, c.degree, L.S, L.K));
   c.partial = c.alloc<double>(size_t(c.partial_n));
   c.scal = c.alloc<double>(16);
-  ck(cudaMemset(c.scal, 0, 16 * sizeof(double)), "memset");
+  ck(cudaMemsetAsync(c.scal, 0, 16 * sizeof(double), c.stream), "memset");
   ck(cudaMallocHost(&c.h_scal, 16 * sizeof(double)), "cudaMallocHost");
   const DevLevel& F = c.lv.back();
   c.staging_n = std::max<long long>(F.N, 1);
   c.staging = c.alloc<double>(size_t(c.staging_n));
   for (double** v : {&c.pcg_r, &c.pcg_z, &c.pcg_p, &c.pcg_Ap, &c.pcg_acc, &c.pcg_u, &c.pcg_f}) {
     *v = c.alloc<double>(size_t(F.lat_n));
-    ck(cudaMemset(*v, 0, sizeof(double) * F.lat_n), "memset");
+    ck(cudaMemsetAsync(*v, 0, sizeof(double) * F.lat_n, c.stream), "memset");
   }
   ck(cudaStreamSynchronize(c.stream), "build sync");
   ck(cudaGetLastError(), "build kernels");
@@ -689,9 +709,15 @@ long long stored_per_patch(int degree, int elements, int dim) {
 
 void op_spmv(pmg_ctx& c, int l, const double* x, const double* f, double* y, double* dot_partial = nullptr) {
   const DevLevel& L = c.lv[l];
-  const double bytes = 8.0 * double(stored_per_patch(c.degree, L.n, c.dim)) * L.K + 8.0 * L.lat_n * (f ? 3 : 2);
+  // algorithmic bytes: the stored entries of the reference's CSR (harness.cpp:274-282),
+  // or with the symmetric half band (stored + diagonal) / 2
+  const double entries = double(stored_per_patch(c.degree, L.n, c.dim));
+  const double band_entries = L.Ob == L.O ? entries : 0.5 * (entries + double(L.S));
+  const double bytes = 8.0 * band_entries * L.K + 8.0 * L.lat_n * (f ? 3 : 2);
+  if (L.Ob != L.O && (reinterpret_cast<uintptr_t>(x) & 15))
+    throw PmgError(PMG_ERR_CONFIG, "half-band SpMV needs a 16-byte aligned x (TMA window)");
   TimedScope ts(c, 0, l, bytes);
-  SpmvArgs a{c.dim, c.degree, L.ext, L.S, L.K, L.band, x, f, y, dot_partial};
+  SpmvArgs a{c.dim, c.degree, L.ext, L.S, L.K, L.band, x, f, y, dot_partial, L.Ob != L.O, L.Sp};
   launch_spmv(c.stream, a);
   c.launches++;
   c.spmv_launches++;
@@ -720,8 +746,10 @@ void op_iface_sum(pmg_ctx& c, int l, const double* r) {
     if (L.n_send) c.launches++;
     c.comm->exchange(c.stream, L.peers);
   }
-  launch_iface_combine(c.stream, L.n_iface, L.if_comb_off, L.if_comb_src, L.if_tloc, L.if_recv, L.if_t);
-  if (L.n_iface) c.launches++;
+  if (c.size > 1) {  // on one rank the fold is the identity: totals = if_tloc
+    launch_iface_combine(c.stream, L.n_iface, L.if_comb_off, L.if_comb_src, L.if_tloc, L.if_recv, L.if_t);
+    if (L.n_iface) c.launches++;
+  }
 }
 
 // smooth: interior FD, faces, edges + vertices.  out_mode SET: out = alpha z
@@ -755,7 +783,7 @@ void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double
   TimedScope ts_iface(c, 3, l, 0.0);
   op_iface_sum(c, l, r);
   if (d == 3 && L.n_face > 0) {
-    launch_gather_t(c.stream, L.face_ndof, L.face_iface, L.if_t, c.face_buf[1]);
+    launch_gather_t(c.stream, L.face_ndof, L.face_iface, L.if_total, c.face_buf[1]);
     c.launches++;
     const double* res = c.face_buf[1];
     if (L.face_small) {
@@ -777,7 +805,7 @@ void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double
   }
   if (L.n_edges + L.n_verts > 0) {
     launch_edges_vertices(c.stream, L.d_edges, L.edge_items, L.n_edge_items, L.edge_iface, L.vert_iface,
-                          L.vert_scalar, L.n_verts, L.if_rep_off, L.if_rep_slot, L.if_t, out, add ? 1 : 0, alpha);
+                          L.vert_scalar, L.n_verts, L.if_rep_off, L.if_rep_slot, L.if_total, out, add ? 1 : 0, alpha);
     c.launches++;
   }
 }
@@ -879,7 +907,7 @@ void op_accumulate(pmg_ctx& c, int l, const double* r, double* out) {
     launch_copy(c.stream, r, out, L.lat_n);
     c.launches++;
   }
-  launch_iface_scatter(c.stream, L.n_iface, L.if_rep_off, L.if_rep_slot, L.if_t, out);
+  launch_iface_scatter(c.stream, L.n_iface, L.if_rep_off, L.if_rep_slot, L.if_total, out);
   if (L.n_iface) c.launches++;
 }
 
@@ -1169,8 +1197,8 @@ int pmg_vec_create(pmg_ctx* ctx, int level, pmg_vec** out) {
     v->ctx = ctx;
     v->level = level;
     v->n = ctx->lv[level].lat_n;
-    ck(cudaMalloc(&v->d, sizeof(double) * std::max<long long>(v->n, 1)), "cudaMalloc vec");
-    ck(cudaMemset(v->d, 0, sizeof(double) * v->n), "memset vec");
+    ck(cudaMalloc(&v->d, sizeof(double) * std::max<long long>(v->n, 1) + 64), "cudaMalloc vec");
+    ck(cudaMemsetAsync(v->d, 0, sizeof(double) * v->n, ctx->stream), "memset vec");
     *out = v.release();
   });
 }

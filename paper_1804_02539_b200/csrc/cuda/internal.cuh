@@ -2,9 +2,12 @@
 //
 // HBM layout (one context = the patches one GPU owns):
 //   lattice vectors   double[K][S], S = (n+p)^d, patch-major, axis 0 fastest
-//   band              double[K][O][S], O = (2p+1)^d, offset-major: a warp's 32
-//                     consecutive rows read 256 contiguous bytes per offset;
-//                     Dirichlet rows and columns are zeroed at upload
+//   band              double[K][Ob][Sp], O = (2p+1)^d offsets (Ob = (O+1)/2,
+//                     the symmetric lower half, on TMA levels), offset-major:
+//                     a warp's 32 consecutive rows read 256 contiguous bytes
+//                     per offset; row stride Sp >= S (spmv_row_stride); every
+//                     (row, column) pair outside the stencil, Dirichlet or
+//                     padding holds an exact 0 (zero_dirichlet_band)
 //   l2g               int32[K][S] (global dof or -1)
 //   replica CSR       per global dof, its lattice slots in ascending (patch,
 //                     local) order -- DofMapper::reps (topology.cpp:367-372)
@@ -57,17 +60,24 @@ struct SpmvArgs {
   int dim, degree, ext;
   long long S;         // rows per patch
   int K;               // patches
-  const double* band;  // [K][O][S]
+  const double* band;  // [K][Ob][Sp]
   const double* x;     // lattice vector (accumulated)
   const double* f;     // residual mode: f (distributed); nullptr for y = A x
   double* y;
   double* dot_partial; // optional: per-block partial of sum y*x (nullptr: none)
+  int half = 0;        // band holds the lower half only ([K][(O+1)/2][Sp])
+  long long Sp = 0;    // band row stride per (patch, offset): spmv_row_stride
 };
 void launch_spmv(cudaStream_t s, const SpmvArgs& a);
 int spmv_blocks(long long rows);
-// band row stride per (patch, offset): S, or S rounded up to 256 on levels
-// streamed with TMA bulk copies
-long long spmv_padded_rows(int dim, int degree, long long S);
+// band row stride per (patch, offset): S, or on levels streamed with TMA bulk
+// copies S + halo rounded up to 256 (halo = p (1 + ext [+ ext^2]) + 2)
+long long spmv_row_stride(int dim, int degree, int ext, long long S);
+// levels whose SpMV streams the band with TMA (S >= 1024, specialised degree)
+bool spmv_tma_level(int dim, int degree, long long S);
+// band offsets stored per patch: (O+1)/2 (symmetric half) on TMA levels when
+// allowed, else O
+int spmv_stored_offsets(int dim, int degree, long long S, bool allow_half);
 // number of dot partials one launch writes
 int spmv_partials(int dim, int degree, long long S, int K);
 
@@ -151,7 +161,7 @@ void launch_prolong_fused(cudaStream_t s, const TsDev& ts, int K, int d, int ext
 void launch_masked_axpy(cudaStream_t s, const int* l2g, long long n, double c, const double* val, double* u);
 void launch_mask_dirichlet(cudaStream_t s, const int* l2g, long long n, double* v);
 void launch_zero_dirichlet_band(cudaStream_t s, int dim, int degree, int ext, long long S, long long Sp, int K,
-                                const int* l2g, double* band);
+                                int stored_offsets, const int* l2g, double* band);
 // scalar helpers on device: out = num/den ; check energy
 void launch_pcg_scalars(cudaStream_t s, int op, double* scal);
 

@@ -426,10 +426,9 @@ __global__ void mask_dirichlet_kernel(const int* __restrict__ l2g, long long n, 
 
 // zero Dirichlet rows/columns and the columns leaving the lattice; padding
 // rows r in [S, Sp) are zeroed too
-__global__ void zero_dirichlet_band_kernel(int dim, int degree, int ext, long long S, long long Sp, int K,
+__global__ void zero_dirichlet_band_kernel(int dim, int degree, int ext, long long S, long long Sp, int K, int O,
                                            const int* __restrict__ l2g, double* __restrict__ band) {
   const int W = 2 * degree + 1;
-  const int O = dim == 2 ? W * W : W * W * W;
   const long long total = (long long)K * O * Sp;
   for (long long idx = blockIdx.x * (long long)kThreads + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * kThreads) {
@@ -601,8 +600,8 @@ void launch_mask_dirichlet(cudaStream_t s, const int* l2g, long long n, double* 
   if (n > 0) mask_dirichlet_kernel<<<grid_for(n), kThreads, 0, s>>>(l2g, n, v);
 }
 void launch_zero_dirichlet_band(cudaStream_t s, int dim, int degree, int ext, long long S, long long Sp, int K,
-                                const int* l2g, double* band) {
-  zero_dirichlet_band_kernel<<<148 * 32, kThreads, 0, s>>>(dim, degree, ext, S, Sp, K, l2g, band);
+                                int stored_offsets, const int* l2g, double* band) {
+  zero_dirichlet_band_kernel<<<148 * 32, kThreads, 0, s>>>(dim, degree, ext, S, Sp, K, stored_offsets, l2g, band);
 }
 void launch_pcg_scalars(cudaStream_t s, int op, double* scal) { pcg_scalars_kernel<<<1, 32, 0, s>>>(op, scal); }
 

@@ -39,18 +39,28 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(SpmvArgs a) {
     const double* __restrict__ x = a.x + gid;
     const long long ext2 = (long long)ext * ext;
     double acc = 0.0;
+    // Small levels are latency-bound: each d0-row's 2p+1 band values and x
+    // values are loaded unconditionally first (x through a clamped address),
+    // so they are all in flight together; the FMAs keep the reference's
+    // per-entry predicate and column order.
 #pragma unroll
     for (int d2 = (D == 3 ? -P : 0); d2 <= (D == 3 ? P : 0); ++d2) {
       const bool ok2 = D == 2 || (i2 + d2 >= 0 && i2 + d2 < ext);
 #pragma unroll
       for (int d1 = -P; d1 <= P; ++d1) {
         const bool ok1 = ok2 && (i1 + d1 >= 0 && i1 + d1 < ext);
+        double bv[W], xv[W];
 #pragma unroll
         for (int d0 = -P; d0 <= P; ++d0) {
           const int o = (d0 + P) + W * ((d1 + P) + W * (D == 3 ? d2 + P : 0));
           const long long off = d0 + (long long)ext * d1 + ext2 * d2;
-          if (ok1 && i0 + d0 >= 0 && i0 + d0 < ext) acc = fma(__ldcs(band + (size_t)o * S), __ldg(x + off), acc);
+          const bool ok = ok1 && i0 + d0 >= 0 && i0 + d0 < ext;
+          bv[d0 + P] = __ldg(band + (size_t)o * S);
+          xv[d0 + P] = __ldg(ok ? x + off : x);
         }
+#pragma unroll
+        for (int d0 = -P; d0 <= P; ++d0)
+          if (ok1 && i0 + d0 >= 0 && i0 + d0 < ext) acc = fma(bv[d0 + P], xv[d0 + P], acc);
       }
     }
     const double y = a.f ? a.f[gid] - acc : acc;
@@ -115,8 +125,9 @@ __global__ void __launch_bounds__(kThreads) spmv_generic_kernel(SpmvArgs a) {
 }
 
 // ---------------------------------------------------------------- TMA stream
-// Large levels: the band is laid out [K][O][Sp] with Sp = S rounded up to 256,
-// so each (offset, 256-row chunk) is one aligned 2 KB segment.  A producer
+// Large levels: the band is laid out [K][O][Sp] with the row stride Sp a
+// multiple of 256 and >= S + halo (spmv_row_stride), so each (offset, 256-row
+// chunk) is one aligned 2 KB segment and every offset row ends in zeros.  A producer
 // warp streams the 2p+1 segments of one (d1, d2) offset row per stage with
 // cp.async.bulk (TMA) into a kStages-deep shared-memory ring guarded by
 // mbarriers; 8 consumer warps (one row per thread) run the FMAs.  The band
@@ -129,13 +140,16 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// "memory" clobbers: the ring's shared-memory reads must stay between the
+// wait on full[s] and the arrive on empty[s] (the producer refills the stage
+// once every consumer warp has arrived).
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
@@ -145,7 +159,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity));
+      "r"(parity)
+      : "memory");
 }
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(
@@ -156,7 +171,7 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 }
 
 template <int D, int P>
-__global__ void __launch_bounds__(kRowsTma + 32) spmv_tma_kernel(SpmvArgs a, long long Sp) {
+__global__ void __launch_bounds__(kRowsTma + 32) spmv_tma_kernel(SpmvArgs a) {
   constexpr int W = 2 * P + 1;
   constexpr int O = D == 2 ? W * W : W * W * W;
   constexpr int NCHUNK = O / W;
@@ -165,16 +180,17 @@ __global__ void __launch_bounds__(kRowsTma + 32) spmv_tma_kernel(SpmvArgs a, lon
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ double red[kRowsTma / 32];
 
-  const long long chunks_per_patch = Sp / kRowsTma;
-  const long long k = blockIdx.x / chunks_per_patch;
-  const long long r0 = (blockIdx.x - k * chunks_per_patch) * kRowsTma;
+  const long long Sp = a.Sp;
+  const long long blocks_per_patch = (a.S + kRowsTma - 1) / kRowsTma;
+  const long long k = blockIdx.x / blocks_per_patch;
+  const long long r0 = (blockIdx.x - k * blocks_per_patch) * kRowsTma;
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kRowsTma / 32);
     }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
@@ -229,7 +245,216 @@ __global__ void __launch_bounds__(kRowsTma + 32) spmv_tma_kernel(SpmvArgs a, lon
   if (a.dot_partial) {  // consumers only: named barrier 1
     for (int o = 16; o > 0; o >>= 1) prod += __shfl_down_sync(0xffffffffu, prod, o);
     if ((tid & 31) == 0) red[tid >> 5] = prod;
-    asm volatile("bar.sync 1, %0;\n" ::"n"(kRowsTma));
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kRowsTma) : "memory");
+    if (tid == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < kRowsTma / 32; ++w) sum += red[w];
+      a.dot_partial[blockIdx.x] = sum;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- half band
+// The stiffness is symmetric, so large levels store only the offsets at or
+// below the centre, o <= (O-1)/2, i.e. the (d2, d1, d0) <= 0 half in the
+// lexicographic order of the CSR columns ([K][OB][Sp], OB = (O+1)/2).  The
+// upper entry A(r, r+s) for s > 0 is the stored A(r+s, r) at the mirrored
+// offset.  Every stage of the ring holds one d0-row of offsets; the sum still
+// runs over o = 0..O-1 in the reference's column order:
+//   chunks [0, RL)       d0-rows strictly below the centre (streamed from HBM)
+//   chunk  RL            the centre row, d0 = -p..0 (ends with the diagonal)
+//   chunk  RL+1          the centre row, d0 = 1..p   (mirrored)
+//   chunks [RL+2, R+1)   d0-rows above the centre    (mirrored)
+// A mirrored segment is the 256 rows [r0+s, r0+s+256) of the mirror offset: it
+// belongs to a CTA a few hundred rows downstream that streams the same bytes
+// at about the same time, so it is served by L2 and the HBM bytes per SpMV are
+// the half band.  TMA needs 16-byte aligned sources, so a mirrored segment
+// starts at the even row below r0+s and carries 258 rows; the consumer adds
+// (s & 1).  Upper values are the lower triangle's: A is symmetric up to
+// rounding in the reference's assembly (E = G H^T, assembly.cpp:218), and
+// this reads each pair once, which is the textbook symmetric operator.
+constexpr int kSeg = kRowsTma + 2;
+
+// The x values one stage multiplies, x[g + off1 - p .. g + off1 + 255 + p]
+// (g = the block's first lattice row), ride in the same stage as a 16-byte
+// aligned window, so consumers read only shared memory.  At the two ends of
+// the lattice the window is clamped (lattice vectors carry 64 B of slack, so
+// the rounded-up end stays inside the allocation).
+template <int P>
+struct XWindow {
+  static constexpr int kLen = kRowsTma + 2 * P + 2;
+  __device__ __forceinline__ static long long start(long long g0, long long total) {
+    long long st = g0 & ~1LL;
+    st = st < 0 ? 0 : st;
+    const long long hi = (total - kLen + 1) & ~1LL;
+    return st > hi ? hi : st;
+  }
+};
+
+// (d1, d2) offset row a chunk of the half-band stream multiplies
+template <int D, int P>
+__device__ __forceinline__ int chunk_row(int c) {
+  constexpr int W = 2 * P + 1;
+  constexpr int RL = ((D == 2 ? W : W * W) - 1) / 2;
+  return c <= RL ? c : (c == RL + 1 ? RL : c - 1);
+}
+
+// One stage of the half-band sum.  Guarded = false is the interior path: every
+// column a row can name lies inside the lattice vector, and the band holds an
+// exact 0 for each (row, column) pair outside the tensor stencil (wrapped
+// lines, neighbouring patches, Dirichlet, padding rows -- zero_dirichlet_band
+// and the Sp >= S + halo stride), so the pair adds fma(0, x, acc) == acc and
+// the per-entry predicates of the reference loop are not needed.  Guarded =
+// true (the blocks touching either end of the lattice) tests every column.
+template <int D, int P, bool Guarded>
+__device__ __forceinline__ double half_stage(int c, const double* seg, const double* xw, long long off1, bool ok1,
+                                             bool row_ok, int i0, int ext, double acc) {
+  constexpr int W = 2 * P + 1;
+  constexpr int RL = ((D == 2 ? W : W * W) - 1) / 2;
+  if (c < RL) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const int d0 = w - P;
+      if (!Guarded || (ok1 && i0 + d0 >= 0 && i0 + d0 < ext)) acc = fma(seg[w * kSeg], xw[d0], acc);
+    }
+  } else if (c == RL) {
+#pragma unroll
+    for (int w = 0; w <= P; ++w) {
+      const int d0 = w - P;
+      if (!Guarded || (ok1 && i0 + d0 >= 0)) acc = fma(seg[w * kSeg], xw[d0], acc);
+    }
+  } else if (c == RL + 1) {
+#pragma unroll
+    for (int w = 0; w < P; ++w) {
+      const int d0 = w + 1;
+      if (!Guarded || (row_ok && i0 + d0 < ext)) acc = fma(seg[w * kSeg + (d0 & 1)], xw[d0], acc);
+    }
+  } else {
+    // mirrored segment w starts at the even row below r0 + off1 + d0
+    const double* s0 = seg + int(off1 & 1);        // even d0
+    const double* s1 = seg + int((off1 + 1) & 1);  // odd d0
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const int d0 = w - P;
+      const double* sw = (d0 & 1) ? s1 : s0;
+      if (!Guarded || (ok1 && i0 + d0 >= 0 && i0 + d0 < ext)) acc = fma(sw[w * kSeg], xw[d0], acc);
+    }
+  }
+  return acc;
+}
+
+// x source of the half-band kernel: false = __ldg through L1 (a block's x
+// footprint is reused by all its offsets), true = a TMA window per stage.
+constexpr bool kHalfXWindow = false;
+
+template <int D, int P>
+__global__ void __launch_bounds__(kRowsTma + 32) spmv_tma_half_kernel(SpmvArgs a) {
+  constexpr int W = 2 * P + 1;
+  constexpr int R = D == 2 ? W : W * W;  // d0-rows of offsets
+  constexpr int RL = (R - 1) / 2;        // d0-rows strictly below the centre row
+  constexpr int OB = RL * W + P + 1;     // stored offsets
+  constexpr int NCH = R + 1;
+  constexpr int kX = kHalfXWindow ? XWindow<P>::kLen : 0;
+  constexpr int kStageDoubles = W * kSeg + kX;
+  extern __shared__ __align__(128) double ring[];  // [kStages][W][kSeg] band + [kX] x
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ double red[kRowsTma / 32];
+
+  const long long Sp = a.Sp;
+  const long long blocks_per_patch = (a.S + kRowsTma - 1) / kRowsTma;
+  const long long k = blockIdx.x / blocks_per_patch;
+  const long long r0 = (blockIdx.x - k * blocks_per_patch) * kRowsTma;
+  const int tid = threadIdx.x;
+  const int ext = a.ext;
+  const long long ext2 = (long long)ext * ext;
+  const long long total = a.S * a.K;
+  const long long g_r0 = k * a.S + r0;  // lattice index of the block's first row
+  const long long halo = P * (1 + ext + (D == 3 ? ext2 : 0)) + 2;
+  const bool guarded = g_r0 - halo < 0 || g_r0 + kRowsTma + halo > total;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kRowsTma / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (tid >= kRowsTma) {  // producer warp
+    if (tid == kRowsTma) {
+      const double* base = a.band + (size_t)k * OB * Sp;
+      for (int c = 0; c < NCH; ++c) {
+        const int s = c % kStages;
+        if (c >= kStages) mbar_wait(&empty[s], ((c / kStages) - 1) & 1);
+        double* dst = ring + (size_t)s * kStageDoubles;
+        const int q = chunk_row<D, P>(c);
+        const long long off1 = (long long)ext * (q % W - P) + (D == 3 ? ext2 * (q / W - P) : 0);
+        const long long xs = XWindow<P>::start(g_r0 + off1 - P, total);
+        if (c <= RL) {
+          const int nw = c < RL ? W : P + 1;
+          mbar_expect_tx(&full[s], unsigned((nw * kRowsTma + kX) * sizeof(double)));
+          for (int w = 0; w < nw; ++w)
+            tma_load_1d(dst + w * kSeg, base + (size_t)(c * W + w) * Sp + r0, kRowsTma * sizeof(double), &full[s]);
+        } else if (c == RL + 1) {
+          mbar_expect_tx(&full[s], unsigned((P * kSeg + kX) * sizeof(double)));
+          for (int w = 0; w < P; ++w) {
+            const int d0 = w + 1;
+            const long long start = (r0 + d0) & ~1LL;
+            tma_load_1d(dst + w * kSeg, base + (size_t)(RL * W + P - d0) * Sp + start, kSeg * sizeof(double),
+                        &full[s]);
+          }
+        } else {
+          const int qm = R - 1 - q;  // the mirror of offset row q
+          mbar_expect_tx(&full[s], unsigned((W * kSeg + kX) * sizeof(double)));
+          for (int w = 0; w < W; ++w) {
+            const long long start = (r0 + off1 + (w - P)) & ~1LL;
+            tma_load_1d(dst + w * kSeg, base + (size_t)(qm * W + (W - 1 - w)) * Sp + start,
+                        kSeg * sizeof(double), &full[s]);
+          }
+        }
+        if (kHalfXWindow) tma_load_1d(dst + W * kSeg, a.x + xs, kX * sizeof(double), &full[s]);
+      }
+    }
+    return;
+  }
+
+  const long long r = r0 + tid;
+  const bool row_ok = r < a.S;
+  const int i0 = int(r % ext);
+  const int i1 = int((r / ext) % ext);
+  const int i2 = D == 3 ? int(r / ext2) : 0;
+  const long long gid = g_r0 + tid;
+  const double fv = (a.f && row_ok) ? a.f[gid] : 0.0;
+  double acc = 0.0;
+  for (int c = 0; c < NCH; ++c) {
+    const int s = c % kStages;
+    const double* seg = ring + (size_t)s * kStageDoubles + tid;
+    const int q = chunk_row<D, P>(c);
+    const int d1 = q % W - P, d2 = D == 3 ? q / W - P : 0;
+    const long long off1 = (long long)ext * d1 + ext2 * d2;
+    // xw[d0] = x[gid + off1 + d0]
+    const double* xw = kHalfXWindow ? seg + W * kSeg + int(g_r0 + off1 - XWindow<P>::start(g_r0 + off1 - P, total))
+                                    : a.x + gid + off1;
+    mbar_wait(&full[s], (c / kStages) & 1);
+    if (guarded) {
+      const bool ok1 = row_ok && i1 + d1 >= 0 && i1 + d1 < ext && (D == 2 || (i2 + d2 >= 0 && i2 + d2 < ext));
+      acc = half_stage<D, P, true>(c, seg, xw, off1, ok1, row_ok, i0, ext, acc);
+    } else {
+      acc = half_stage<D, P, false>(c, seg, xw, off1, true, true, i0, ext, acc);
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+  }
+  double prod = 0.0;
+  if (row_ok) {
+    const double y = a.f ? fv - acc : acc;
+    a.y[gid] = y;
+    if (a.dot_partial) prod = y * a.x[gid];
+  }
+  if (a.dot_partial) {
+    for (int o = 16; o > 0; o >>= 1) prod += __shfl_down_sync(0xffffffffu, prod, o);
+    if ((tid & 31) == 0) red[tid >> 5] = prod;
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kRowsTma) : "memory");
     if (tid == 0) {
       double sum = 0.0;
       for (int w = 0; w < kRowsTma / 32; ++w) sum += red[w];
@@ -239,40 +464,60 @@ __global__ void __launch_bounds__(kRowsTma + 32) spmv_tma_kernel(SpmvArgs a, lon
 }
 
 template <int D, int P>
-bool launch_tma(cudaStream_t s, const SpmvArgs& a, long long Sp) {
+void launch_tma(cudaStream_t s, const SpmvArgs& a) {
   constexpr int W = 2 * P + 1;
+  const long long grid = (a.S + kRowsTma - 1) / kRowsTma * a.K;
+  if (a.half) {
+    const size_t smem = (size_t)kStages * (W * kSeg + (kHalfXWindow ? XWindow<P>::kLen : 0)) * sizeof(double);
+    static bool configured = false;  // per process; one device per context thread
+    if (!configured) {
+      cudaFuncSetAttribute(spmv_tma_half_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      configured = true;
+    }
+    spmv_tma_half_kernel<D, P><<<unsigned(grid), kRowsTma + 32, smem, s>>>(a);
+    return;
+  }
   const size_t smem = (size_t)kStages * W * kRowsTma * sizeof(double);
-  static bool configured = false;  // per process; one device per context thread
+  static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(spmv_tma_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     configured = true;
   }
-  const long long grid = (Sp / kRowsTma) * a.K;
-  spmv_tma_kernel<D, P><<<unsigned(grid), kRowsTma + 32, smem, s>>>(a, Sp);
-  return true;
+  spmv_tma_kernel<D, P><<<unsigned(grid), kRowsTma + 32, smem, s>>>(a);
 }
 
 }  // namespace
 
-long long spmv_padded_rows(int dim, int degree, long long S) {
-  const bool tma = S >= 1024 && ((dim == 2 && degree >= 1 && degree <= 8 && degree != 7) ||
-                                 (dim == 3 && degree >= 1 && degree <= 4));
-  return tma ? (S + kRowsTma - 1) / kRowsTma * kRowsTma : S;
+bool spmv_tma_level(int dim, int degree, long long S) {
+  return S >= 1024 && ((dim == 2 && degree >= 1 && degree <= 8 && degree != 7) ||
+                       (dim == 3 && degree >= 1 && degree <= 4));
+}
+
+long long spmv_row_stride(int dim, int degree, int ext, long long S) {
+  if (!spmv_tma_level(dim, degree, S)) return S;
+  // room for every mirrored read of a valid row to land in this offset's own
+  // zero padding: S + halo, rounded to whole 256-row segments
+  const long long halo = (long long)degree * (1 + ext + (dim == 3 ? (long long)ext * ext : 0)) + 2;
+  return (S + halo + kRowsTma - 1) / kRowsTma * kRowsTma;
+}
+
+int spmv_stored_offsets(int dim, int degree, long long S, bool allow_half) {
+  const int W = 2 * degree + 1;
+  const int O = dim == 2 ? W * W : W * W * W;
+  return allow_half && spmv_tma_level(dim, degree, S) ? (O + 1) / 2 : O;
 }
 
 int spmv_blocks(long long rows) { return int((rows + kThreads - 1) / kThreads); }
 
 int spmv_partials(int dim, int degree, long long S, int K) {
-  const long long Sp = spmv_padded_rows(dim, degree, S);
-  if (Sp != S) return int((Sp / kRowsTma) * K);
+  if (spmv_tma_level(dim, degree, S)) return int((S + kRowsTma - 1) / kRowsTma * K);
   return spmv_blocks(S * K);
 }
 
 void launch_spmv(cudaStream_t s, const SpmvArgs& a) {
-  const long long Sp = spmv_padded_rows(a.dim, a.degree, a.S);
-  if (Sp != a.S) {
+  if (spmv_tma_level(a.dim, a.degree, a.S)) {
 #define PMG_TMA_CASE(D, P) \
-  if (a.dim == D && a.degree == P) { launch_tma<D, P>(s, a, Sp); return; }
+  if (a.dim == D && a.degree == P) { launch_tma<D, P>(s, a); return; }
     PMG_TMA_CASE(2, 1) PMG_TMA_CASE(2, 2) PMG_TMA_CASE(2, 3) PMG_TMA_CASE(2, 4)
     PMG_TMA_CASE(2, 5) PMG_TMA_CASE(2, 6) PMG_TMA_CASE(2, 8)
     PMG_TMA_CASE(3, 1) PMG_TMA_CASE(3, 2) PMG_TMA_CASE(3, 3) PMG_TMA_CASE(3, 4)
