@@ -129,6 +129,12 @@ struct pmg_ctx {
          *pcg_u = nullptr, *pcg_f = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
+  // the interface pieces of a smooth run on side_stream, concurrent with the
+  // interior FD (they write disjoint slots); fork/join by events, so the
+  // overlap is captured into the CUDA graphs too.  PMG_NO_OVERLAP=1 disables.
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool overlap = true;
   std::vector<void*> allocs;
   size_t bytes = 0;
   long long launches = 0, spmv_launches = 0;
@@ -216,6 +222,9 @@ struct pmg_ctx {
     if (graph_front) cudaGraphExecDestroy(graph_front);
     if (graph_back) cudaGraphExecDestroy(graph_back);
     if (ev_norm) cudaEventDestroy(ev_norm);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side_stream) cudaStreamDestroy(side_stream);
     for (auto& t : timed) {
       cudaEventDestroy(t.a);
       cudaEventDestroy(t.b);
@@ -754,10 +763,30 @@ void op_iface_sum(pmg_ctx& c, int l, const double* r) {
 
 // smooth: interior FD, faces, edges + vertices.  out_mode SET: out = alpha z
 // on every piece slot; ADD: out += alpha z.
+void op_smooth_iface(pmg_ctx& c, int l, const double* r, double* out, bool add, double alpha);
+
 void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double alpha) {
   const DevLevel& L = c.lv[l];
   const int d = c.dim;
   const int np = 2 * d;
+  // interface pieces first, on the side stream when overlapping
+  const cudaStream_t main = c.stream;
+  const bool fork = c.overlap && !c.profiling && L.n_int > 0;
+  if (fork) {
+    ck(cudaEventRecord(c.ev_fork, main), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(c.side_stream, c.ev_fork, 0), "cudaStreamWaitEvent");
+    c.stream = c.side_stream;
+  }
+  try {
+    op_smooth_iface(c, l, r, out, add, alpha);
+  } catch (...) {
+    c.stream = main;
+    throw;
+  }
+  if (fork) {
+    ck(cudaEventRecord(c.ev_join, c.side_stream), "cudaEventRecord");
+    c.stream = main;
+  }
   if (L.int_small) {
     double flops = 0.0;
     for (int pass = 0; pass < np; ++pass) flops += fd_pass_flops(L, L.int_dims, d, pass);
@@ -776,6 +805,12 @@ void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double
                    alpha, c.work[(pass + 1) & 1], c.work[pass & 1]);
     if (L.n_int_items[pass]) c.launches++;
   }
+  if (fork) ck(cudaStreamWaitEvent(main, c.ev_join, 0), "cudaStreamWaitEvent");
+}
+
+void op_smooth_iface(pmg_ctx& c, int l, const double* r, double* out, bool add, double alpha) {
+  const DevLevel& L = c.lv[l];
+  const int d = c.dim;
   // interface pieces act on the summed residual: Sigma over every replica
   // (all ranks), then each rank solves the pieces it touches and writes its
   // local replicas (ParallelBackend::smooth = accumulate(apply_pieces(r)),
@@ -1120,6 +1155,13 @@ int pmg_ctx_create(const pmg_hierarchy_desc* desc, int device, const pmg_comm_de
     ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own_stream;
     ck(cudaEventCreateWithFlags(&c->ev_norm, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "cudaEventCreate");
+    {
+      const char* e = std::getenv("PMG_NO_OVERLAP");
+      c->overlap = !(e && e[0] == '1');
+    }
     build_ctx(*c, *desc);
   } catch (const PmgError& e) {
     g_create_error = e.what();

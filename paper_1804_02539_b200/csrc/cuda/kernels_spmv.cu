@@ -13,6 +13,7 @@
 // The row's sum runs over the offsets in the reference CSR column order
 // (axis 0 fastest).
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -488,8 +489,20 @@ void launch_tma(cudaStream_t s, const SpmvArgs& a) {
 
 }  // namespace
 
+// Every level of a specialised degree streams its band with TMA: on small
+// levels the one-thread-per-row loop is latency-bound (each thread walks its
+// (2p+1)^d entries with few loads in flight), while the staged stream keeps a
+// whole block's band in flight.  PMG_TMA_MIN_ROWS raises the threshold.
+static long long tma_min_rows() {
+  static const long long v = [] {
+    const char* e = std::getenv("PMG_TMA_MIN_ROWS");
+    return e ? std::atoll(e) : 0LL;
+  }();
+  return v;
+}
+
 bool spmv_tma_level(int dim, int degree, long long S) {
-  return S >= 1024 && ((dim == 2 && degree >= 1 && degree <= 8 && degree != 7) ||
+  return S >= tma_min_rows() && ((dim == 2 && degree >= 1 && degree <= 8 && degree != 7) ||
                        (dim == 3 && degree >= 1 && degree <= 4));
 }
 
