@@ -67,6 +67,7 @@ struct DevLevel {
   int n_int = 0;
   int4* int_items[6] = {};
   int n_int_items[6] = {};
+  int int_ntc[6] = {};
   std::vector<std::array<int, 3>> int_dims;  // host copy for flop counts
   bool int_small = false, face_small = false;  // whole solve per CTA in shared memory
   long long int_max_total = 0, face_max_total = 0;
@@ -78,6 +79,7 @@ struct DevLevel {
   long long face_ndof = 0;
   int4* face_items[4] = {};
   int n_face_items[4] = {};
+  int face_ntc[4] = {};
   // edges / vertices
   EdgePiece* d_edges = nullptr;
   int n_edges = 0;
@@ -550,6 +552,13 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
                 L.int_max_total <= small_max;
   L.face_small = 2 * L.face_max_total + (long long)maxdim_face * maxdim_face <= kFdSmallDoubles &&
                  L.face_max_total <= small_max;
+  // pieces ordered so that equal (dims, factors) are adjacent
+  auto piece_key = [&](const FdPiece& a) {
+    return std::make_tuple(a.dims[0], a.dims[1], a.dims[2], a.B[0][0], a.B[1][0], a.B[2][0]);
+  };
+  auto by_key = [&](const FdPiece& a, const FdPiece& b) { return piece_key(a) < piece_key(b); };
+  std::stable_sort(h_int.begin(), h_int.end(), by_key);
+  std::stable_sort(h_face.begin(), h_face.end(), by_key);
   L.n_int = int(h_int.size());
   L.d_int = c.upload(h_int);
   L.n_face = int(h_face.size());
@@ -569,23 +578,54 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   L.n_verts = int(vert_g.size());
   L.vert_iface = c.upload(vert_g);
   L.vert_scalar = c.upload(vert_scalar);
-  // CTA work items of every pass: (piece, row panel, column panel)
-  auto make_items = [&](const std::vector<FdPiece>& ps, int naxes, int4** items, int* counts) {
-    const int BM = fd_rows_per_block(), BN = fd_cols_per_block();
+  // CTA work items of every pass.  Pieces with the same dims and the same
+  // factor for the pass form a group whose rows are concatenated (no per-piece
+  // row padding); items = (first piece, row panel, column panel, group rows).
+  auto make_items = [&](const std::vector<FdPiece>& ps, int naxes, int4** items, int* counts, int* ntcs) {
+    const int BM = fd_rows_per_block();
     for (int pass = 0; pass < 2 * naxes; ++pass) {
-      std::vector<int4> it;
+      const int axis = pass % naxes, dir = pass / naxes;
+      std::vector<std::pair<int, int>> groups;  // (first, count)
+      static const bool group_pieces = [] {
+        const char* e = std::getenv("PMG_FD_GROUP");
+        return !(e && e[0] == '0');
+      }();
       for (int i = 0; i < int(ps.size()); ++i) {
-        const int K = ps[i].dims[pass % naxes];
-        const long long R = ps[i].total / K;
-        for (long long r0 = 0; r0 < R; r0 += BM)
-          for (int n0 = 0; n0 < K; n0 += BN) it.push_back(make_int4(i, int(r0), n0, 0));
+        bool same = group_pieces && !groups.empty();
+        if (same) {
+          const FdPiece& a = ps[groups.back().first];
+          const FdPiece& b = ps[i];
+          for (int x = 0; x < naxes; ++x) same = same && a.dims[x] == b.dims[x];
+          same = same && a.B[axis][dir] == b.B[axis][dir];
+        }
+        if (same)
+          groups.back().second++;
+        else
+          groups.push_back({i, 1});
+      }
+      std::vector<long long> cols, weight;
+      for (const auto& gr : groups) {
+        cols.push_back(ps[gr.first].dims[axis]);
+        weight.push_back(ps[gr.first].total * gr.second / ps[gr.first].dims[axis]);
+      }
+      const char* fntc = std::getenv("PMG_FD_NTC");
+      const int ntc = fntc ? std::atoi(fntc) : fd_pick_ntc(cols.data(), weight.data(), int(groups.size()));
+      const int BN = 8 * ntc;
+      std::vector<int4> it;
+      for (const auto& gr : groups) {
+        const int K = ps[gr.first].dims[axis];
+        const long long rows = ps[gr.first].total / K * gr.second;
+        if (rows > INT32_MAX) throw PmgError(PMG_ERR_CONFIG, "FD piece group too large");
+        for (long long r0 = 0; r0 < rows; r0 += BM)
+          for (int n0 = 0; n0 < K; n0 += BN) it.push_back(make_int4(gr.first, int(r0), n0, int(rows)));
       }
       counts[pass] = int(it.size());
       items[pass] = c.upload(it);
+      ntcs[pass] = ntc;
     }
   };
-  make_items(h_int, d, L.int_items, L.n_int_items);
-  if (d == 3) make_items(h_face, 2, L.face_items, L.n_face_items);
+  make_items(h_int, d, L.int_items, L.n_int_items, L.int_ntc);
+  if (d == 3) make_items(h_face, 2, L.face_items, L.n_face_items, L.face_ntc);
 
   // ---- two-scale factor (TransferOperator ctor, transfer.cpp:10-19)
   if (l >= 1) {
@@ -801,7 +841,8 @@ void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double
     if (pass == d - 1) out_mode = FD_OUT_WORK_DIAG;
     if (pass == np - 1) out_mode = add ? FD_OUT_LATTICE_ADD : FD_OUT_LATTICE_SET;
     TimedScope ts(c, 1, l, fd_pass_flops(L, L.int_dims, d, pass));
-    launch_fd_pass(c.stream, L.d_int, L.int_items[pass], L.n_int_items[pass], pass, d, in_mode, out_mode, r, out,
+    launch_fd_pass(c.stream, L.d_int, L.int_items[pass], L.n_int_items[pass], L.int_ntc[pass], pass, d, in_mode,
+                   out_mode, r, out,
                    alpha, c.work[(pass + 1) & 1], c.work[pass & 1]);
     if (L.n_int_items[pass]) c.launches++;
   }
@@ -829,7 +870,8 @@ void op_smooth_iface(pmg_ctx& c, int l, const double* r, double* out, bool add, 
     } else {
       for (int pass = 0; pass < 4; ++pass) {
         const int out_mode = pass == 1 ? FD_OUT_WORK_DIAG : FD_OUT_WORK;
-        launch_fd_pass(c.stream, L.d_face, L.face_items[pass], L.n_face_items[pass], pass, 2, FD_IN_WORK, out_mode,
+        launch_fd_pass(c.stream, L.d_face, L.face_items[pass], L.n_face_items[pass], L.face_ntc[pass], pass, 2,
+                       FD_IN_WORK, out_mode,
                        nullptr, nullptr, 0.0, c.face_buf[(pass + 1) & 1], c.face_buf[pass & 1]);
         c.launches++;
       }

@@ -24,6 +24,38 @@ namespace pmgcu {
 
 constexpr int kThreads = 256;
 
+// ---------------------------------------------------------------- launches
+// Every kernel is launched with programmatic stream serialization (PDL): the
+// next kernel in the stream is scheduled while this one runs, and waits in
+// PMG_PDL_ENTRY (griddepcontrol.wait) until its predecessor has completed
+// and flushed, so dependent kernels pay no launch gap.  A kernel reads no
+// global data before PMG_PDL_ENTRY; completion is transitive, so waiting on
+// the direct predecessor orders it after everything earlier in the stream.
+// PMG_NO_PDL=1 launches without the attribute (the wait is then a no-op).
+#define PMG_PDL_ENTRY()                                           \
+  do {                                                            \
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");           \
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); \
+  } while (0)
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  static_assert(sizeof...(KArgs) == sizeof...(Args), "kernel argument count");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- FD
 struct FdPiece {
   int dims[3];
@@ -41,11 +73,14 @@ enum FdOut { FD_OUT_WORK = 0, FD_OUT_WORK_DIAG = 1, FD_OUT_LATTICE_SET = 2, FD_O
 
 // One fast-diagonalization pass (contract one axis, rotate the layout).
 // items: (piece, first row, first column, 0) per CTA.
-void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int pass, int naxes,
-                    int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
+// items: (first piece of a group of pieces sharing dims and factor, first row
+// of the panel within the group, first column, rows of the group); ntc = the
+// column-panel width in 8-column tiles (fd_pick_ntc)
+void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int ntc, int pass,
+                    int naxes, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
                     const double* work_in, double* work_out);
 int fd_rows_per_block();
-int fd_cols_per_block();
+int fd_pick_ntc(const long long* cols, const long long* weight, int n);
 void fd_configure();  // per device, before the first pass
 // whole solve of every piece in one launch, one CTA per piece, tensor and one
 // factor in shared memory: 2 max_total + max_dim^2 doubles <= kFdSmallDoubles

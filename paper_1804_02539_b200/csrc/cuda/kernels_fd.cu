@@ -31,13 +31,19 @@ namespace {
 constexpr int kFdThreads = 128;
 constexpr int kBM = 32;          // rows per CTA (4 warps x 8)
 constexpr int kBK = 16;          // k per shared-memory stage
-constexpr int kNTC = 9;          // n-tiles (of 8 columns) per CTA
-constexpr int kBN = 8 * kNTC;    // 72 columns per CTA
 constexpr int kXS = kBK + 4;     // X row stride (doubles): conflict-free A fragments
-constexpr int kBS = 84;          // B row stride: round_up(72, 16) + 4, conflict-free B fragments
 constexpr int kStagesFd = 3;
 constexpr int kXPer = kBM * kBK / kFdThreads;  // 4 X copies per thread and stage
-constexpr int kBPer = kBK * kBN / kFdThreads;  // 9 B copies per thread and stage
+
+// column panel of NTC n-tiles (8 columns each); B row stride = 4 mod 16
+// doubles so the 4 x 8 B-fragment reads of a half-warp hit distinct banks
+template <int NTC>
+struct FdTile {
+  static constexpr int BN = 8 * NTC;
+  static constexpr int BS = (BN + 11) / 16 * 16 + 4;
+  static constexpr int BPer = (kBK * BN + kFdThreads - 1) / kFdThreads;
+  static constexpr size_t smem = sizeof(double) * kStagesFd * (kBM * kXS + kBK * BS);
+};
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -55,6 +61,11 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// One pass over a group of pieces with the same dims and the same factor B
+// (pieces are independent; a group's rows are concatenated so the M
+// dimension has no per-piece padding).  item = (first piece of the group,
+// first row of the panel within the group, first column, rows of the group).
+template <int NTC>
 __global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece* __restrict__ pieces,
                                                                   const int4* __restrict__ items, int pass,
                                                                   int naxes, int in_mode, int out_mode,
@@ -62,20 +73,24 @@ __global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece*
                                                                   double* __restrict__ lat_out, double alpha,
                                                                   const double* __restrict__ work_in,
                                                                   double* __restrict__ work_out) {
-  __shared__ __align__(16) double Xs[kStagesFd][kBM * kXS];
-  __shared__ __align__(16) double Bs[kStagesFd][kBK * kBS];
-  const int4 it = items[blockIdx.x];  // (piece, first row, first column, -)
-  const FdPiece& P = pieces[it.x];
+  PMG_PDL_ENTRY();
+  using T = FdTile<NTC>;
+  extern __shared__ __align__(16) double fd_smem[];  // Xs[kStagesFd][kBM * kXS], Bs[kStagesFd][kBK * BS]
+  auto Xs = reinterpret_cast<double(*)[kBM * kXS]>(fd_smem);
+  auto Bs = reinterpret_cast<double(*)[kBK * T::BS]>(fd_smem + kStagesFd * kBM * kXS);
+  const int4 it = items[blockIdx.x];
+  const FdPiece& P0 = pieces[it.x];
   const int axis = pass % naxes;
   const int dir = pass / naxes;
-  const int K = P.dims[axis];
+  const int K = P0.dims[axis];
   const int N = K;
-  const long long R = P.total / K;
+  const long long R = P0.total / K;  // rows per piece
+  const long long rows = it.w;       // rows of the group
   const long long r0 = it.y;
   const int n0 = it.z;
-  const int m0 = P.dims[0], m1 = P.dims[1];
-  const long long ext = P.ext, ext2 = (long long)P.ext * P.ext;
-  const double* __restrict__ B = P.B[axis][dir];
+  const int m0 = P0.dims[0], m1 = P0.dims[1];
+  const long long ext = P0.ext, ext2 = (long long)P0.ext * P0.ext;
+  const double* __restrict__ B = P0.B[axis][dir];
   const int tid = threadIdx.x;
 
   // per-thread copy plan: X element (rr, kk) = (tid/16 + 8j, tid%16); B element
@@ -86,23 +101,25 @@ __global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece*
 #pragma unroll
   for (int j = 0; j < kXPer; ++j) {
     const long long r = r0 + tid / kBK + 8 * j;
-    xrow_ok[j] = r < R;
-    const long long rr = xrow_ok[j] ? r : 0;
+    xrow_ok[j] = r < rows;
+    const long long rg = xrow_ok[j] ? r : 0;
+    const FdPiece& P = pieces[it.x + int(rg / R)];
+    const long long rr = rg % R;
     if (in_mode == FD_IN_WORK)
       xsrc[j] = work_in + P.work_off + rr * K + xk;
     else
       xsrc[j] = lat_in + P.lat_base + (naxes == 3 ? ext * (rr % m1) + ext2 * (rr / m1) : ext * rr) + xk;
   }
-  int boff[kBPer], bkk[kBPer], bdst[kBPer];
-  bool bn_ok[kBPer];
+  int boff[T::BPer], bkk[T::BPer], bdst[T::BPer];
+  bool bn_ok[T::BPer];
 #pragma unroll
-  for (int j = 0; j < kBPer; ++j) {
+  for (int j = 0; j < T::BPer; ++j) {
     const int idx = tid + kFdThreads * j;
-    const int nn = idx % kBN, kk = idx / kBN;
-    bn_ok[j] = n0 + nn < N;
+    const int nn = idx % T::BN, kk = idx / T::BN;
+    bn_ok[j] = n0 + nn < N && kk < kBK;
     bkk[j] = kk;
     boff[j] = kk * N + n0 + nn;
-    bdst[j] = kk * kBS + nn;
+    bdst[j] = kk * T::BS + nn;
   }
   auto load = [&](int stage, int k0) {
     double* xs = Xs[stage];
@@ -113,17 +130,38 @@ __global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece*
       cp_async8(xs + (tid / kBK + 8 * j) * kXS + xk, ok ? xsrc[j] + k0 : B, ok);
     }
 #pragma unroll
-    for (int j = 0; j < kBPer; ++j) {
+    for (int j = 0; j < T::BPer; ++j) {
+      if (bkk[j] >= kBK) continue;
       const bool ok = bn_ok[j] && k0 + bkk[j] < K;
       cp_async8(bs + bdst[j], ok ? B + boff[j] + (long long)k0 * N : B, ok);
     }
   };
 
+  // epilogues that read global data (the diagonal, or u for u += tau z) pull
+  // their lines into L2 now, so the reads after the main loop hit L2: per
+  // column, the panel's 32 rows are 256 contiguous bytes
+  if (out_mode == FD_OUT_WORK_DIAG || out_mode == FD_OUT_LATTICE_ADD) {
+    const long long rl0 = r0 % R;
+    const FdPiece& Pf = pieces[it.x + int(r0 / R)];
+    for (int idx = tid; idx < 2 * T::BN; idx += kFdThreads) {
+      const int n = n0 + idx / 2;
+      if (n >= N) continue;
+      const double* a;
+      if (out_mode == FD_OUT_WORK_DIAG) {
+        a = Pf.diag + rl0 + R * n;
+      } else {
+        const long long lr = naxes == 3 ? (rl0 % m0) + ext * (rl0 / m0) : rl0;
+        a = lat_out + Pf.lat_base + lr + (naxes == 3 ? ext2 : ext) * n;
+      }
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a + 16 * (idx & 1)));
+    }
+  }
+
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  double acc[kNTC][2];
+  double acc[NTC][2];
 #pragma unroll
-  for (int j = 0; j < kNTC; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int j = 0; j < NTC; ++j) acc[j][0] = acc[j][1] = 0.0;
 
   const int nst = (K + kBK - 1) / kBK;
 #pragma unroll
@@ -141,35 +179,50 @@ __global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece*
       cp_async_commit();
     }
     const double* xs = Xs[cur] + (warp * 8 + g) * kXS + t;
-    const double* bs = Bs[cur] + t * kBS + g;
+    const double* bs = Bs[cur] + t * T::BS + g;
+    // fragments of k-step ks + 1 are read while k-step ks multiplies
+    double af[2], bf[2][NTC];
+    af[0] = xs[0];
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) bf[0][j] = bs[j * 8];
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
-      const double a = xs[ks * 4];
+      const int c = ks & 1;
+      if (ks + 1 < kBK / 4) {
+        af[c ^ 1] = xs[(ks + 1) * 4];
 #pragma unroll
-      for (int j = 0; j < kNTC; ++j) dmma(acc[j][0], acc[j][1], a, bs[ks * 4 * kBS + j * 8]);
+        for (int j = 0; j < NTC; ++j) bf[c ^ 1][j] = bs[(ks + 1) * 4 * T::BS + j * 8];
+      }
+#pragma unroll
+      for (int j = 0; j < NTC; ++j) dmma(acc[j][0], acc[j][1], af[c], bf[c][j]);
     }
   }
 
-  // epilogue: lane holds rows r0+8w+g, columns n0+8j+2t+{0,1}; Y(r,n) at r + R n
+  // epilogue: lane holds row r0+8w+g of the group, columns n0+8j+2t+{0,1};
+  // within its piece, Y(rl, n) at rl + R n
   const long long r = r0 + warp * 8 + g;
-  if (r >= R) return;
+  if (r >= rows) return;
+  const FdPiece& P = pieces[it.x + int(r / R)];
+  const long long rl = r % R;
   long long lat_row = 0;
-  if (out_mode >= FD_OUT_LATTICE_SET) lat_row = P.lat_base + (naxes == 3 ? (r % m0) + ext * (r / m0) : r);
+  if (out_mode >= FD_OUT_LATTICE_SET) lat_row = P.lat_base + (naxes == 3 ? (rl % m0) + ext * (rl / m0) : rl);
   const long long lat_stride = naxes == 3 ? ext2 : ext;
+  double* __restrict__ wout = work_out + P.work_off;
+  const double* __restrict__ diag = P.diag;
 #pragma unroll
-  for (int j = 0; j < kNTC; ++j) {
+  for (int j = 0; j < NTC; ++j) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int n = n0 + j * 8 + 2 * t + i;
       if (n >= N) continue;
       const double v = acc[j][i];
-      const long long o = r + R * n;
+      const long long o = rl + R * n;
       switch (out_mode) {
         case FD_OUT_WORK:
-          work_out[P.work_off + o] = v;
+          wout[o] = v;
           break;
         case FD_OUT_WORK_DIAG:
-          work_out[P.work_off + o] = v / P.diag[o];
+          wout[o] = v / diag[o];
           break;
         case FD_OUT_LATTICE_SET:
           lat_out[lat_row + lat_stride * n] = alpha * v;
@@ -238,6 +291,7 @@ __global__ void __launch_bounds__(kSmallThreads) fd_small_kernel(const FdPiece* 
                                                                  double* __restrict__ lat_out, double alpha,
                                                                  const double* __restrict__ work_in,
                                                                  double* __restrict__ work_out) {
+  PMG_PDL_ENTRY();
   extern __shared__ double sm[];
   const FdPiece& P = pieces[blockIdx.x];
   const int dims[3] = {P.dims[0], P.dims[1], naxes == 3 ? P.dims[2] : 1};
@@ -303,23 +357,50 @@ void launch_fd_small(cudaStream_t s, const FdPiece* pieces, int npieces, int nax
                      const double* work_in, double* work_out) {
   if (npieces == 0) return;
   const size_t smem = fd_small_smem(max_total, max_dim);
-  fd_small_kernel<<<npieces, kSmallThreads, smem, s>>>(pieces, naxes, in_mode, out_mode, lat_in, lat_out, alpha,
+  launch_k(fd_small_kernel, dim3(npieces), dim3(kSmallThreads), smem, s, pieces, naxes, in_mode, out_mode, lat_in, lat_out, alpha,
                                                        work_in, work_out);
 }
 
 void fd_configure() {
   cudaFuncSetAttribute(fd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(fd_pass_dmma_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<5>::smem));
+  cudaFuncSetAttribute(fd_pass_dmma_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<9>::smem));
+  cudaFuncSetAttribute(fd_pass_dmma_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<11>::smem));
 }
 
 int fd_rows_per_block() { return kBM; }
-int fd_cols_per_block() { return kBN; }
 
-void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int pass, int naxes,
-                    int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
+int fd_pick_ntc(const long long* cols, const long long* weight, int n) {
+  // the column-panel width (in n-tiles) with the least padding over the
+  // groups; 11 (88 columns) is measured slower than 9 at the c2 finest level
+  // (fewer, larger CTAs per wave) and is only used when forced (PMG_FD_NTC)
+  static const int cands[2] = {5, 9};
+  int best = 9;
+  double best_cost = -1.0;
+  for (int c : cands) {
+    double cost = 0.0;
+    for (int i = 0; i < n; ++i) cost += double(weight[i]) * double((cols[i] + 8 * c - 1) / (8 * c) * (8 * c));
+    if (best_cost < 0.0 || cost < best_cost || (cost == best_cost && c > best)) {
+      best = c;
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
+void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int ntc, int pass,
+                    int naxes, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
                     const double* work_in, double* work_out) {
   if (nitems == 0) return;
-  fd_pass_dmma_kernel<<<nitems, kFdThreads, 0, s>>>(pieces, items, pass, naxes, in_mode, out_mode, lat_in, lat_out,
-                                                    alpha, work_in, work_out);
+#define PMG_FD_CASE(NT)                                                                                          \
+  if (ntc == NT) {                                                                                               \
+    launch_k(fd_pass_dmma_kernel<NT>, dim3(nitems), dim3(kFdThreads), FdTile<NT>::smem, s, pieces, items, pass,  \
+             naxes, in_mode,                                                                                     \
+             out_mode, lat_in, lat_out, alpha, work_in, work_out);                                               \
+    return;                                                                                                      \
+  }
+  PMG_FD_CASE(5) PMG_FD_CASE(9) PMG_FD_CASE(11)
+#undef PMG_FD_CASE
 }
 
 }  // namespace pmgcu

@@ -4,6 +4,8 @@
 // All of these are HBM- or latency-bound.  Reductions use a fixed grid and a
 // fixed-order final sum, so every result is bitwise reproducible run to run
 // (the property the reference gets from ascending-rank sums, parallel.hpp:26-30).
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace pmgcu {
@@ -16,11 +18,13 @@ inline int grid_for(long long n, int per_thread = 1) {
 }
 
 __global__ void fill_kernel(double* x, long long n, double v) {
+  PMG_PDL_ENTRY();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     x[i] = v;
 }
 
 __global__ void copy_kernel(const double* __restrict__ x, double* __restrict__ y, long long n) {
+  PMG_PDL_ENTRY();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     y[i] = x[i];
 }
@@ -28,6 +32,7 @@ __global__ void copy_kernel(const double* __restrict__ x, double* __restrict__ y
 // y += a x  (axpy_acc / axpy_dist, multigrid.hpp:108-109); a from device when given
 __global__ void axpy_kernel(double a, const double* a_dev, double sign, const double* __restrict__ x,
                             double* __restrict__ y, long long n) {
+  PMG_PDL_ENTRY();
   const double s = a_dev ? sign * a_dev[0] : a;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     y[i] += s * x[i];
@@ -36,12 +41,14 @@ __global__ void axpy_kernel(double a, const double* a_dev, double sign, const do
 // p = z + beta p  (xpay_acc, multigrid.hpp:110)
 __global__ void xpay_kernel(const double* __restrict__ z, double beta, const double* beta_dev, double* __restrict__ p,
                             long long n) {
+  PMG_PDL_ENTRY();
   const double b = beta_dev ? beta_dev[0] : beta;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = z[i] + b * p[i];
 }
 
 __global__ void scale_set_kernel(double a, const double* __restrict__ x, double* __restrict__ y, long long n) {
+  PMG_PDL_ENTRY();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     y[i] = a * x[i];
 }
@@ -59,6 +66,7 @@ __device__ inline double block_sum(double v) {
 
 __global__ void dot_partial_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
                                    double* __restrict__ partial) {
+  PMG_PDL_ENTRY();
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kThreads)
     s += a[i] * b[i];
@@ -67,6 +75,7 @@ __global__ void dot_partial_kernel(const double* __restrict__ a, const double* _
 }
 
 __global__ void sum_partials_kernel(const double* __restrict__ partial, int n, double* out) {
+  PMG_PDL_ENTRY();
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += kThreads) s += partial[i];
   s = block_sum(s);
@@ -78,6 +87,7 @@ __global__ void sum_partials_kernel(const double* __restrict__ partial, int n, d
 // of MultiPatchOperator::apply, assembly.cpp:276-277)
 __global__ void group_sum_kernel(const int* __restrict__ goff, const int* __restrict__ gslot, int ngroups,
                                  const double* __restrict__ r, double* __restrict__ out) {
+  PMG_PDL_ENTRY();
   const int g = blockIdx.x * kThreads + threadIdx.x;
   if (g >= ngroups) return;
   double s = 0.0;
@@ -88,6 +98,7 @@ __global__ void group_sum_kernel(const int* __restrict__ goff, const int* __rest
 __global__ void gather_sum_kernel(const int* __restrict__ dof_g, long long ndof, const int* __restrict__ rep_off,
                                   const int* __restrict__ rep_slot, const double* __restrict__ r,
                                   double* __restrict__ buf) {
+  PMG_PDL_ENTRY();
   const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
   if (i >= ndof) return;
   const int g = dof_g[i];
@@ -99,6 +110,7 @@ __global__ void gather_sum_kernel(const int* __restrict__ dof_g, long long ndof,
 __global__ void scatter_kernel(const int* __restrict__ dof_g, long long ndof, const int* __restrict__ rep_off,
                                const int* __restrict__ rep_slot, const double* __restrict__ buf,
                                double* __restrict__ out, int add, double alpha) {
+  PMG_PDL_ENTRY();
   const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
   if (i >= ndof) return;
   const int g = dof_g[i];
@@ -121,6 +133,7 @@ __global__ void __launch_bounds__(kThreads) edges_vertices_kernel(
     const int* __restrict__ edge_iface, const int* __restrict__ vert_iface, const double* __restrict__ vert_scalar,
     int nverts, const int* __restrict__ rep_off, const int* __restrict__ rep_slot, const double* __restrict__ t,
     double* __restrict__ out, int add, double alpha) {
+  PMG_PDL_ENTRY();
   // t: interface totals (sum over every replica, all ranks); rep_off/rep_slot:
   // this rank's replicas of each interface dof
   __shared__ double buf[512];
@@ -174,6 +187,7 @@ __global__ void __launch_bounds__(kThreads) edges_vertices_kernel(
 __global__ void lattice_from_global_kernel(const int* __restrict__ l2g, const unsigned char* __restrict__ owner,
                                            long long n, int form, const double* __restrict__ g,
                                            double* __restrict__ lat) {
+  PMG_PDL_ENTRY();
   const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
   if (i >= n) return;
   const int d = l2g[i];
@@ -185,6 +199,7 @@ __global__ void lattice_from_global_kernel(const int* __restrict__ l2g, const un
 __global__ void global_from_lattice_kernel(const int* __restrict__ rep_off, const int* __restrict__ rep_slot,
                                            long long ndofs, int form, const double* __restrict__ lat,
                                            double* __restrict__ g) {
+  PMG_PDL_ENTRY();
   const long long d = blockIdx.x * (long long)kThreads + threadIdx.x;
   if (d >= ndofs) return;
   if (form == 0) {  // dofs without a replica on this rank read as 0
@@ -198,6 +213,7 @@ __global__ void global_from_lattice_kernel(const int* __restrict__ rep_off, cons
 
 __global__ void coarse_gather_kernel(const int* __restrict__ rep_off, const int* __restrict__ rep_slot, int n0,
                                      const double* __restrict__ r, double* __restrict__ rhs) {
+  PMG_PDL_ENTRY();
   const int d = blockIdx.x * kThreads + threadIdx.x;
   if (d >= n0) return;
   double s = 0.0;
@@ -208,6 +224,7 @@ __global__ void coarse_gather_kernel(const int* __restrict__ rep_off, const int*
 // x = Ainv rhs, one warp per row, fixed lane-strided order + shuffle tree
 __global__ void coarse_gemv_kernel(const double* __restrict__ Ainv, int n0, const double* __restrict__ rhs,
                                    double* __restrict__ x) {
+  PMG_PDL_ENTRY();
   const int warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n0) return;
@@ -220,6 +237,7 @@ __global__ void coarse_gemv_kernel(const double* __restrict__ Ainv, int n0, cons
 
 __global__ void coarse_scatter_kernel(const int* __restrict__ l2g, long long n, const double* __restrict__ x,
                                       double* __restrict__ out) {
+  PMG_PDL_ENTRY();
   const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
   if (i >= n) return;
   const int d = l2g[i];
@@ -234,6 +252,7 @@ __global__ void coarse_scatter_kernel(const int* __restrict__ l2g, long long n, 
 __global__ void ts_axis_kernel(TsDev ts, int transpose, int K, int d, int in0, int in1, int in2, int axis,
                                const double* __restrict__ in, double* __restrict__ out, int mode,
                                const int* __restrict__ l2g, double coef) {
+  PMG_PDL_ENTRY();
   int dims_in[3] = {in0, in1, in2};
   int dims_out[3] = {in0, in1, in2};
   dims_out[axis] = transpose ? ts.coarse_dim : ts.fine_dim;
@@ -272,6 +291,7 @@ __global__ void ts_axis_kernel(TsDev ts, int transpose, int K, int d, int in0, i
 // T_loc[i] = sum of this rank's replicas of interface dof i (ascending slot)
 __global__ void iface_partial_kernel(int n, const int* __restrict__ rep_off, const int* __restrict__ rep_slot,
                                      const double* __restrict__ r, double* __restrict__ tloc) {
+  PMG_PDL_ENTRY();
   const int i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
@@ -281,6 +301,7 @@ __global__ void iface_partial_kernel(int n, const int* __restrict__ rep_off, con
 
 __global__ void iface_pack_kernel(int n, const int* __restrict__ idx, const double* __restrict__ tloc,
                                   double* __restrict__ send) {
+  PMG_PDL_ENTRY();
   const int q = blockIdx.x * kThreads + threadIdx.x;
   if (q < n) send[q] = tloc[idx[q]];
 }
@@ -289,6 +310,7 @@ __global__ void iface_pack_kernel(int n, const int* __restrict__ idx, const doub
 __global__ void iface_combine_kernel(int n, const int* __restrict__ comb_off, const int* __restrict__ comb_src,
                                      const double* __restrict__ tloc, const double* __restrict__ recv,
                                      double* __restrict__ t) {
+  PMG_PDL_ENTRY();
   const int i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
@@ -301,6 +323,7 @@ __global__ void iface_combine_kernel(int n, const int* __restrict__ comb_off, co
 
 __global__ void iface_scatter_kernel(int n, const int* __restrict__ rep_off, const int* __restrict__ rep_slot,
                                      const double* __restrict__ t, double* __restrict__ out) {
+  PMG_PDL_ENTRY();
   const int i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   const double v = t[i];
@@ -309,6 +332,7 @@ __global__ void iface_scatter_kernel(int n, const int* __restrict__ rep_off, con
 
 __global__ void gather_t_kernel(long long n, const int* __restrict__ map, const double* __restrict__ t,
                                 double* __restrict__ buf) {
+  PMG_PDL_ENTRY();
   const long long j = blockIdx.x * (long long)kThreads + threadIdx.x;
   if (j < n) buf[j] = t[map[j]];
 }
@@ -316,6 +340,7 @@ __global__ void gather_t_kernel(long long n, const int* __restrict__ map, const 
 __global__ void scatter_iface_kernel(long long n, const int* __restrict__ map, const int* __restrict__ rep_off,
                                      const int* __restrict__ rep_slot, const double* __restrict__ buf,
                                      double* __restrict__ out, int add, double alpha) {
+  PMG_PDL_ENTRY();
   const long long j = blockIdx.x * (long long)kThreads + threadIdx.x;
   if (j >= n) return;
   const int i = map[j];
@@ -330,6 +355,7 @@ __global__ void scatter_iface_kernel(long long n, const int* __restrict__ map, c
 
 // ascending-rank sums: out[d] = sum_r parts[r * n + d]
 __global__ void sum_ranks_kernel(const double* __restrict__ parts, int ranks, int n, double* __restrict__ out) {
+  PMG_PDL_ENTRY();
   const int d = blockIdx.x * kThreads + threadIdx.x;
   if (d >= n) return;
   double s = 0.0;
@@ -345,6 +371,7 @@ __global__ void sum_ranks_kernel(const double* __restrict__ parts, int ranks, in
 // the <= p+1 parents per axis, on non-Dirichlet fine slots.
 __global__ void restrict_fused_kernel(TsDev ts, int K, int d, int ext_f, int ext_c, const double* __restrict__ r,
                                       double* __restrict__ out, const int* __restrict__ l2g_c) {
+  PMG_PDL_ENTRY();
   long long Sc = 1, Sf = 1;
   for (int a = 0; a < d; ++a) {
     Sc *= ext_c;
@@ -380,6 +407,7 @@ __global__ void restrict_fused_kernel(TsDev ts, int K, int d, int ext_f, int ext
 
 __global__ void prolong_fused_kernel(TsDev ts, int K, int d, int ext_f, int ext_c, const double* __restrict__ c,
                                      double coef, double* __restrict__ u, const int* __restrict__ l2g_f) {
+  PMG_PDL_ENTRY();
   long long Sc = 1, Sf = 1;
   for (int a = 0; a < d; ++a) {
     Sc *= ext_c;
@@ -413,12 +441,14 @@ __global__ void prolong_fused_kernel(TsDev ts, int K, int d, int ext_f, int ext_
 
 __global__ void masked_axpy_kernel(const int* __restrict__ l2g, long long n, double c, const double* __restrict__ val,
                                    double* __restrict__ u) {
+  PMG_PDL_ENTRY();
   const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
   if (i >= n) return;
   if (l2g[i] >= 0) u[i] += c * val[i];
 }
 
 __global__ void mask_dirichlet_kernel(const int* __restrict__ l2g, long long n, double* __restrict__ v) {
+  PMG_PDL_ENTRY();
   const long long i = blockIdx.x * (long long)kThreads + threadIdx.x;
   if (i >= n) return;
   if (l2g[i] < 0) v[i] = 0.0;
@@ -428,6 +458,7 @@ __global__ void mask_dirichlet_kernel(const int* __restrict__ l2g, long long n, 
 // rows r in [S, Sp) are zeroed too
 __global__ void zero_dirichlet_band_kernel(int dim, int degree, int ext, long long S, long long Sp, int K, int O,
                                            const int* __restrict__ l2g, double* __restrict__ band) {
+  PMG_PDL_ENTRY();
   const int W = 2 * degree + 1;
   const long long total = (long long)K * O * Sp;
   for (long long idx = blockIdx.x * (long long)kThreads + threadIdx.x; idx < total;
@@ -454,6 +485,7 @@ __global__ void zero_dirichlet_band_kernel(int dim, int degree, int ext, long lo
 
 // PCG scalars kept on device: [0] rz [1] pAp [2] alpha [3] rz_next [4] beta [5] |r|^2 [6] |r| [7] flag
 __global__ void pcg_scalars_kernel(int op, double* s) {
+  PMG_PDL_ENTRY();
   if (threadIdx.x != 0) return;
   switch (op) {
     case 0:  // alpha = rz / pAp; flag non-positive energy
@@ -472,20 +504,28 @@ __global__ void pcg_scalars_kernel(int op, double* s) {
 
 }  // namespace
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PMG_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 void launch_fill(cudaStream_t s, double* x, long long n, double v) {
-  if (n > 0) fill_kernel<<<grid_for(n, 4), kThreads, 0, s>>>(x, n, v);
+  if (n > 0) launch_k(fill_kernel, dim3(grid_for(n, 4)), dim3(kThreads), 0, s, x, n, v);
 }
 void launch_copy(cudaStream_t s, const double* x, double* y, long long n) {
-  if (n > 0) copy_kernel<<<grid_for(n, 4), kThreads, 0, s>>>(x, y, n);
+  if (n > 0) launch_k(copy_kernel, dim3(grid_for(n, 4)), dim3(kThreads), 0, s, x, y, n);
 }
 void launch_axpy(cudaStream_t s, double a, const double* a_dev, double sign, const double* x, double* y, long long n) {
-  if (n > 0) axpy_kernel<<<grid_for(n, 4), kThreads, 0, s>>>(a, a_dev, sign, x, y, n);
+  if (n > 0) launch_k(axpy_kernel, dim3(grid_for(n, 4)), dim3(kThreads), 0, s, a, a_dev, sign, x, y, n);
 }
 void launch_xpay(cudaStream_t s, const double* z, double beta, const double* beta_dev, double* p, long long n) {
-  if (n > 0) xpay_kernel<<<grid_for(n, 4), kThreads, 0, s>>>(z, beta, beta_dev, p, n);
+  if (n > 0) launch_k(xpay_kernel, dim3(grid_for(n, 4)), dim3(kThreads), 0, s, z, beta, beta_dev, p, n);
 }
 void launch_scale_set(cudaStream_t s, double a, const double* x, double* y, long long n) {
-  if (n > 0) scale_set_kernel<<<grid_for(n, 4), kThreads, 0, s>>>(a, x, y, n);
+  if (n > 0) launch_k(scale_set_kernel, dim3(grid_for(n, 4)), dim3(kThreads), 0, s, a, x, y, n);
 }
 int dot_blocks(long long n) {
   long long g = (n + kThreads * 8 - 1) / (kThreads * 8);
@@ -493,22 +533,22 @@ int dot_blocks(long long n) {
   return int(g < 1 ? 1 : g);
 }
 void launch_dot_partial(cudaStream_t s, const double* a, const double* b, long long n, double* partial) {
-  dot_partial_kernel<<<dot_blocks(n), kThreads, 0, s>>>(a, b, n, partial);
+  launch_k(dot_partial_kernel, dim3(dot_blocks(n)), dim3(kThreads), 0, s, a, b, n, partial);
 }
 void launch_sum_partials(cudaStream_t s, const double* partial, int nparts, double* out) {
-  sum_partials_kernel<<<1, kThreads, 0, s>>>(partial, nparts, out);
+  launch_k(sum_partials_kernel, dim3(1), dim3(kThreads), 0, s, partial, nparts, out);
 }
 void launch_group_sum(cudaStream_t s, const int* goff, const int* gslot, int ngroups, const double* r, double* out) {
-  if (ngroups > 0) group_sum_kernel<<<grid_for(ngroups), kThreads, 0, s>>>(goff, gslot, ngroups, r, out);
+  if (ngroups > 0) launch_k(group_sum_kernel, dim3(grid_for(ngroups)), dim3(kThreads), 0, s, goff, gslot, ngroups, r, out);
 }
 void launch_gather_sum(cudaStream_t s, const int* dof_g, long long ndof, const int* rep_off, const int* rep_slot,
                        const double* r, double* buf) {
-  if (ndof > 0) gather_sum_kernel<<<grid_for(ndof), kThreads, 0, s>>>(dof_g, ndof, rep_off, rep_slot, r, buf);
+  if (ndof > 0) launch_k(gather_sum_kernel, dim3(grid_for(ndof)), dim3(kThreads), 0, s, dof_g, ndof, rep_off, rep_slot, r, buf);
 }
 void launch_scatter(cudaStream_t s, const int* dof_g, long long ndof, const int* rep_off, const int* rep_slot,
                     const double* buf, double* out, int add, double alpha) {
   if (ndof > 0)
-    scatter_kernel<<<grid_for(ndof), kThreads, 0, s>>>(dof_g, ndof, rep_off, rep_slot, buf, out, add, alpha);
+    launch_k(scatter_kernel, dim3(grid_for(ndof)), dim3(kThreads), 0, s, dof_g, ndof, rep_off, rep_slot, buf, out, add, alpha);
 }
 void launch_edges_vertices(cudaStream_t s, const EdgePiece* edges, const int2* items, int nitems,
                            const int* edge_dof_g, const int* vert_g, const double* vert_scalar, int nverts,
@@ -516,34 +556,34 @@ void launch_edges_vertices(cudaStream_t s, const EdgePiece* edges, const int2* i
                            double alpha) {
   const int grid = nitems + (nverts > 0 ? 1 : 0);
   if (grid > 0)
-    edges_vertices_kernel<<<grid, kThreads, 0, s>>>(edges, items, nitems, edge_dof_g, vert_g, vert_scalar, nverts,
+    launch_k(edges_vertices_kernel, dim3(grid), dim3(kThreads), 0, s, edges, items, nitems, edge_dof_g, vert_g, vert_scalar, nverts,
                                                     rep_off, rep_slot, r, out, add, alpha);
 }
 void launch_lattice_from_global(cudaStream_t s, const int* l2g, const unsigned char* owner, long long n, int form,
                                 const double* g, double* lat) {
-  if (n > 0) lattice_from_global_kernel<<<grid_for(n), kThreads, 0, s>>>(l2g, owner, n, form, g, lat);
+  if (n > 0) launch_k(lattice_from_global_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, l2g, owner, n, form, g, lat);
 }
 void launch_global_from_lattice(cudaStream_t s, const int* rep_off, const int* rep_slot, long long ndofs, int form,
                                 const double* lat, double* g) {
-  if (ndofs > 0) global_from_lattice_kernel<<<grid_for(ndofs), kThreads, 0, s>>>(rep_off, rep_slot, ndofs, form, lat, g);
+  if (ndofs > 0) launch_k(global_from_lattice_kernel, dim3(grid_for(ndofs)), dim3(kThreads), 0, s, rep_off, rep_slot, ndofs, form, lat, g);
 }
 void launch_coarse(cudaStream_t s, const int* rep_off, const int* rep_slot, const int* l2g, int n0, long long lat_n,
                    const double* Ainv, const double* r, double* rhs, double* x, double* out) {
   if (n0 > 0) {
-    coarse_gather_kernel<<<grid_for(n0), kThreads, 0, s>>>(rep_off, rep_slot, n0, r, rhs);
-    coarse_gemv_kernel<<<grid_for((long long)n0 * 32), kThreads, 0, s>>>(Ainv, n0, rhs, x);
+    launch_k(coarse_gather_kernel, dim3(grid_for(n0)), dim3(kThreads), 0, s, rep_off, rep_slot, n0, r, rhs);
+    launch_k(coarse_gemv_kernel, dim3(grid_for((long long)n0 * 32)), dim3(kThreads), 0, s, Ainv, n0, rhs, x);
   }
-  coarse_scatter_kernel<<<grid_for(lat_n), kThreads, 0, s>>>(l2g, lat_n, x, out);
+  launch_k(coarse_scatter_kernel, dim3(grid_for(lat_n)), dim3(kThreads), 0, s, l2g, lat_n, x, out);
 }
 void launch_coarse_gather(cudaStream_t s, const int* rep_off, const int* rep_slot, int n0, const double* r,
                           double* rhs) {
-  if (n0 > 0) coarse_gather_kernel<<<grid_for(n0), kThreads, 0, s>>>(rep_off, rep_slot, n0, r, rhs);
+  if (n0 > 0) launch_k(coarse_gather_kernel, dim3(grid_for(n0)), dim3(kThreads), 0, s, rep_off, rep_slot, n0, r, rhs);
 }
 void launch_coarse_gemv(cudaStream_t s, const double* Ainv, int n0, const double* rhs, double* x) {
-  if (n0 > 0) coarse_gemv_kernel<<<grid_for((long long)n0 * 32), kThreads, 0, s>>>(Ainv, n0, rhs, x);
+  if (n0 > 0) launch_k(coarse_gemv_kernel, dim3(grid_for((long long)n0 * 32)), dim3(kThreads), 0, s, Ainv, n0, rhs, x);
 }
 void launch_coarse_scatter(cudaStream_t s, const int* l2g, long long lat_n, const double* x, double* out) {
-  coarse_scatter_kernel<<<grid_for(lat_n), kThreads, 0, s>>>(l2g, lat_n, x, out);
+  launch_k(coarse_scatter_kernel, dim3(grid_for(lat_n)), dim3(kThreads), 0, s, l2g, lat_n, x, out);
 }
 void launch_ts_axis(cudaStream_t s, const TsDev& ts, bool transpose, int K, int d, const int* in_dims, int axis,
                     const double* in, double* out, int mode, const int* l2g, double coef) {
@@ -552,57 +592,57 @@ void launch_ts_axis(cudaStream_t s, const TsDev& ts, bool transpose, int K, int 
   const long long total = per_out * K;
   long long g = (total + kThreads - 1) / kThreads;
   if (g > 148LL * 32) g = 148LL * 32;
-  ts_axis_kernel<<<int(g < 1 ? 1 : g), kThreads, 0, s>>>(ts, transpose ? 1 : 0, K, d, in_dims[0], in_dims[1],
+  launch_k(ts_axis_kernel, dim3(int(g < 1 ? 1 : g)), dim3(kThreads), 0, s, ts, transpose ? 1 : 0, K, d, in_dims[0], in_dims[1],
                                                          d == 3 ? in_dims[2] : 1, axis, in, out, mode, l2g, coef);
 }
 void launch_iface_partial(cudaStream_t s, int n, const int* rep_off, const int* rep_slot, const double* r,
                           double* tloc) {
-  if (n > 0) iface_partial_kernel<<<grid_for(n), kThreads, 0, s>>>(n, rep_off, rep_slot, r, tloc);
+  if (n > 0) launch_k(iface_partial_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, n, rep_off, rep_slot, r, tloc);
 }
 void launch_iface_pack(cudaStream_t s, int n, const int* idx, const double* tloc, double* send) {
-  if (n > 0) iface_pack_kernel<<<grid_for(n), kThreads, 0, s>>>(n, idx, tloc, send);
+  if (n > 0) launch_k(iface_pack_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, n, idx, tloc, send);
 }
 void launch_iface_combine(cudaStream_t s, int n, const int* comb_off, const int* comb_src, const double* tloc,
                           const double* recv, double* t) {
-  if (n > 0) iface_combine_kernel<<<grid_for(n), kThreads, 0, s>>>(n, comb_off, comb_src, tloc, recv, t);
+  if (n > 0) launch_k(iface_combine_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, n, comb_off, comb_src, tloc, recv, t);
 }
 void launch_iface_scatter(cudaStream_t s, int n, const int* rep_off, const int* rep_slot, const double* t,
                           double* out) {
-  if (n > 0) iface_scatter_kernel<<<grid_for(n), kThreads, 0, s>>>(n, rep_off, rep_slot, t, out);
+  if (n > 0) launch_k(iface_scatter_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, n, rep_off, rep_slot, t, out);
 }
 void launch_gather_t(cudaStream_t s, long long n, const int* map, const double* t, double* buf) {
-  if (n > 0) gather_t_kernel<<<grid_for(n), kThreads, 0, s>>>(n, map, t, buf);
+  if (n > 0) launch_k(gather_t_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, n, map, t, buf);
 }
 void launch_scatter_iface(cudaStream_t s, long long n, const int* map, const int* rep_off, const int* rep_slot,
                           const double* buf, double* out, int add, double alpha) {
   if (n > 0)
-    scatter_iface_kernel<<<grid_for(n), kThreads, 0, s>>>(n, map, rep_off, rep_slot, buf, out, add, alpha);
+    launch_k(scatter_iface_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, n, map, rep_off, rep_slot, buf, out, add, alpha);
 }
 void launch_sum_ranks(cudaStream_t s, const double* parts, int ranks, int n, double* out) {
-  if (n > 0) sum_ranks_kernel<<<grid_for(n), kThreads, 0, s>>>(parts, ranks, n, out);
+  if (n > 0) launch_k(sum_ranks_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, parts, ranks, n, out);
 }
 void launch_restrict_fused(cudaStream_t s, const TsDev& ts, int K, int d, int ext_f, int ext_c, const double* r,
                            double* out, const int* l2g_c) {
   long long n = K;
   for (int a = 0; a < d; ++a) n *= ext_c;
-  restrict_fused_kernel<<<grid_for(n), kThreads, 0, s>>>(ts, K, d, ext_f, ext_c, r, out, l2g_c);
+  launch_k(restrict_fused_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, ts, K, d, ext_f, ext_c, r, out, l2g_c);
 }
 void launch_prolong_fused(cudaStream_t s, const TsDev& ts, int K, int d, int ext_f, int ext_c, const double* c,
                           double coef, double* u, const int* l2g_f) {
   long long n = K;
   for (int a = 0; a < d; ++a) n *= ext_f;
-  prolong_fused_kernel<<<grid_for(n), kThreads, 0, s>>>(ts, K, d, ext_f, ext_c, c, coef, u, l2g_f);
+  launch_k(prolong_fused_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, ts, K, d, ext_f, ext_c, c, coef, u, l2g_f);
 }
 void launch_masked_axpy(cudaStream_t s, const int* l2g, long long n, double c, const double* val, double* u) {
-  if (n > 0) masked_axpy_kernel<<<grid_for(n), kThreads, 0, s>>>(l2g, n, c, val, u);
+  if (n > 0) launch_k(masked_axpy_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, l2g, n, c, val, u);
 }
 void launch_mask_dirichlet(cudaStream_t s, const int* l2g, long long n, double* v) {
-  if (n > 0) mask_dirichlet_kernel<<<grid_for(n), kThreads, 0, s>>>(l2g, n, v);
+  if (n > 0) launch_k(mask_dirichlet_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, l2g, n, v);
 }
 void launch_zero_dirichlet_band(cudaStream_t s, int dim, int degree, int ext, long long S, long long Sp, int K,
                                 int stored_offsets, const int* l2g, double* band) {
-  zero_dirichlet_band_kernel<<<148 * 32, kThreads, 0, s>>>(dim, degree, ext, S, Sp, K, stored_offsets, l2g, band);
+  launch_k(zero_dirichlet_band_kernel, dim3(148 * 32), dim3(kThreads), 0, s, dim, degree, ext, S, Sp, K, stored_offsets, l2g, band);
 }
-void launch_pcg_scalars(cudaStream_t s, int op, double* scal) { pcg_scalars_kernel<<<1, 32, 0, s>>>(op, scal); }
+void launch_pcg_scalars(cudaStream_t s, int op, double* scal) { launch_k(pcg_scalars_kernel, dim3(1), dim3(32), 0, s, op, scal); }
 
 }  // namespace pmgcu

@@ -23,6 +23,7 @@ namespace {
 
 template <int D, int P>
 __global__ void __launch_bounds__(kThreads) spmv_kernel(SpmvArgs a) {
+  PMG_PDL_ENTRY();
   constexpr int W = 2 * P + 1;
   constexpr int O = D == 2 ? W * W : W * W * W;
   const long long S = a.S;
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(SpmvArgs a) {
 
 // Runtime-degree fallback (degrees without a specialisation).
 __global__ void __launch_bounds__(kThreads) spmv_generic_kernel(SpmvArgs a) {
+  PMG_PDL_ENTRY();
   const int D = a.dim, P = a.degree, W = 2 * P + 1;
   const int O = D == 2 ? W * W : W * W * W;
   const long long S = a.S;
@@ -173,6 +175,7 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 
 template <int D, int P>
 __global__ void __launch_bounds__(kRowsTma + 32) spmv_tma_kernel(SpmvArgs a) {
+  PMG_PDL_ENTRY();
   constexpr int W = 2 * P + 1;
   constexpr int O = D == 2 ? W * W : W * W * W;
   constexpr int NCHUNK = O / W;
@@ -350,6 +353,7 @@ constexpr bool kHalfXWindow = false;
 
 template <int D, int P>
 __global__ void __launch_bounds__(kRowsTma + 32) spmv_tma_half_kernel(SpmvArgs a) {
+  PMG_PDL_ENTRY();
   constexpr int W = 2 * P + 1;
   constexpr int R = D == 2 ? W : W * W;  // d0-rows of offsets
   constexpr int RL = (R - 1) / 2;        // d0-rows strictly below the centre row
@@ -475,7 +479,7 @@ void launch_tma(cudaStream_t s, const SpmvArgs& a) {
       cudaFuncSetAttribute(spmv_tma_half_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       configured = true;
     }
-    spmv_tma_half_kernel<D, P><<<unsigned(grid), kRowsTma + 32, smem, s>>>(a);
+    launch_k(spmv_tma_half_kernel<D, P>, dim3(unsigned(grid)), dim3(kRowsTma + 32), smem, s, a);
     return;
   }
   const size_t smem = (size_t)kStages * W * kRowsTma * sizeof(double);
@@ -484,7 +488,7 @@ void launch_tma(cudaStream_t s, const SpmvArgs& a) {
     cudaFuncSetAttribute(spmv_tma_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     configured = true;
   }
-  spmv_tma_kernel<D, P><<<unsigned(grid), kRowsTma + 32, smem, s>>>(a);
+  launch_k(spmv_tma_kernel<D, P>, dim3(unsigned(grid)), dim3(kRowsTma + 32), smem, s, a);
 }
 
 }  // namespace
@@ -539,12 +543,12 @@ void launch_spmv(cudaStream_t s, const SpmvArgs& a) {
   const int grid = spmv_blocks(a.S * a.K);
   if (grid == 0) return;
 #define PMG_SPMV_CASE(D, P) \
-  if (a.dim == D && a.degree == P) { spmv_kernel<D, P><<<grid, kThreads, 0, s>>>(a); return; }
+  if (a.dim == D && a.degree == P) { launch_k(spmv_kernel<D, P>, dim3(grid), dim3(kThreads), 0, s, a); return; }
   PMG_SPMV_CASE(2, 1) PMG_SPMV_CASE(2, 2) PMG_SPMV_CASE(2, 3) PMG_SPMV_CASE(2, 4)
   PMG_SPMV_CASE(2, 5) PMG_SPMV_CASE(2, 6) PMG_SPMV_CASE(2, 8)
   PMG_SPMV_CASE(3, 1) PMG_SPMV_CASE(3, 2) PMG_SPMV_CASE(3, 3) PMG_SPMV_CASE(3, 4)
 #undef PMG_SPMV_CASE
-  spmv_generic_kernel<<<grid, kThreads, 0, s>>>(a);
+  launch_k(spmv_generic_kernel, dim3(grid), dim3(kThreads), 0, s, a);
 }
 
 }  // namespace pmgcu
