@@ -70,7 +70,8 @@ void pmg_ctx_destroy(pmg_ctx* ctx);
 /* Message of the last failure on ctx (or of the last failed create when NULL). */
 const char* pmg_last_error(pmg_ctx* ctx);
 /* what: 0 finest level, 1 lattice slots of level `level`, 2 device bytes held,
- *       3 num_dofs of level `level`, 4 local patches.  level = what >> 8. */
+ *       3 num_dofs of level `level`, 4 local patches, 5 microseconds spent in
+ *       device stiffness assembly (PMG_BAND_ASSEMBLE levels).  level = what >> 8. */
 int pmg_ctx_info(pmg_ctx* ctx, int what, int64_t* out);
 /* Launch everything on this cudaStream_t from now on (NULL: the ctx stream). */
 int pmg_set_stream(pmg_ctx* ctx, void* stream);

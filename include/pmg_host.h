@@ -35,6 +35,11 @@ enum {
  * Level l has n0 * 2^l elements per patch direction, l = 0..levels. */
 int pmgh_build(const char* domain, int split, int degree, int n0, int levels, const pmg_cycle_params* params,
                int rhs_kind, uint64_t seed, int threads, pmgh_hierarchy** out);
+/* flags: PMGH_DEVICE_ASSEMBLY leaves the stiffness of levels >= 1 unassembled
+ * (PMG_BAND_ASSEMBLE): the CUDA context assembles it from the patch geometry. */
+enum { PMGH_DEVICE_ASSEMBLY = 1 };
+int pmgh_build_ex(const char* domain, int split, int degree, int n0, int levels, const pmg_cycle_params* params,
+                  int rhs_kind, uint64_t seed, int threads, int flags, pmgh_hierarchy** out);
 void pmgh_free(pmgh_hierarchy* h);
 const char* pmgh_last_error(void);
 

@@ -41,10 +41,23 @@ enum {
 enum { PMG_PIECE_INTERIOR = 0, PMG_PIECE_FACE = 1, PMG_PIECE_EDGE = 2, PMG_PIECE_VERTEX = 3 };
 
 /* Stiffness storage of one level.
- *   PMG_BAND_TENSOR: index-free band[k][o][r], o = sum_a (delta_a+p)(2p+1)^a,
- *                    zero where the column leaves the patch lattice.
- *   PMG_BAND_CSR:    the reference PatchOperator triple per patch. */
-enum { PMG_BAND_TENSOR = 0, PMG_BAND_CSR = 1 };
+ *   PMG_BAND_TENSOR:   index-free band[k][o][r], o = sum_a (delta_a+p)(2p+1)^a,
+ *                      zero where the column leaves the patch lattice.
+ *   PMG_BAND_CSR:      the reference PatchOperator triple per patch.
+ *   PMG_BAND_ASSEMBLE: no values; the context assembles the band on the device
+ *                      from pmg_hierarchy_desc.geometry (assemble_patch_stiffness,
+ *                      assembly.cpp:127-248, with Gauss-Legendre p+1 points). */
+enum { PMG_BAND_TENSOR = 0, PMG_BAND_CSR = 1, PMG_BAND_ASSEMBLE = 2 };
+
+/* Geometry of one patch (GeometryMap, geometry.hpp): a tensor B-spline map
+ * whose axis a uses the uniform open-knot space of degree[a] with elements[a]
+ * elements (free ends); ctrl holds prod(elements[a]+degree[a]) control points
+ * of dim coordinates each, axis 0 fastest. */
+typedef struct {
+  int degree[3];
+  int elements[3];
+  const double* ctrl;
+} pmg_patch_geometry;
 
 typedef struct {
   int nu;
@@ -102,6 +115,8 @@ typedef struct {
   int coarse_n;
   const double* coarse_A; /* dense, column-major */
   const double* coarse_L; /* lower Cholesky factor of coarse_A, column-major */
+  /* per patch; required when a level uses PMG_BAND_ASSEMBLE, else may be NULL */
+  const pmg_patch_geometry* geometry;
 } pmg_hierarchy_desc;
 
 #ifdef __cplusplus

@@ -37,11 +37,20 @@ class PmgLevelDesc(C.Structure):
     ]
 
 
+class PmgPatchGeometry(C.Structure):
+    _fields_ = [("degree", C.c_int * 3), ("elements", C.c_int * 3), ("ctrl", C.POINTER(C.c_double))]
+
+
+PMG_BAND_TENSOR, PMG_BAND_CSR, PMG_BAND_ASSEMBLE = 0, 1, 2
+PMGH_DEVICE_ASSEMBLY = 1
+
+
 class PmgHierarchyDesc(C.Structure):
     _fields_ = [
         ("dim", C.c_int), ("degree", C.c_int), ("num_patches", C.c_int), ("num_levels", C.c_int),
         ("params", PmgCycleParams), ("levels", C.POINTER(PmgLevelDesc)),
         ("coarse_n", C.c_int), ("coarse_A", C.POINTER(C.c_double)), ("coarse_L", C.POINTER(C.c_double)),
+        ("geometry", C.POINTER(PmgPatchGeometry)),
     ]
 
 
@@ -97,6 +106,9 @@ def host_lib():
         lib = C.CDLL(str(path))
         _sig(lib, "pmgh_build", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(PmgCycleParams),
                                           C.c_int, C.c_uint64, C.c_int, C.POINTER(_vp)])
+        _sig(lib, "pmgh_build_ex", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             C.POINTER(PmgCycleParams), C.c_int, C.c_uint64, C.c_int, C.c_int,
+                                             C.POINTER(_vp)])
         _sig(lib, "pmgh_free", None, [_vp])
         _sig(lib, "pmgh_last_error", C.c_char_p, [])
         _sig(lib, "pmgh_describe", C.c_int, [_vp, C.POINTER(PmgHierarchyDesc)])

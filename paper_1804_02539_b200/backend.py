@@ -108,6 +108,12 @@ class GpuBackend:
     def finest_level(self) -> int:
         return self.h.finest_level
 
+    def assembly_seconds(self) -> float:
+        """Wall time of device stiffness assembly at context creation (0 if none)."""
+        n = C.c_int64()
+        self._check(self._lib.pmg_ctx_info(self._ctx, 5, C.byref(n)))
+        return n.value / 1e6
+
     def lattice_size(self, level: int) -> int:
         n = C.c_int64()
         self._check(self._lib.pmg_ctx_info(self._ctx, (level << 8) | 1, C.byref(n)))

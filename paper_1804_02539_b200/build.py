@@ -19,7 +19,9 @@ LIB = PKG / "lib"
 ORACLE_BUILD = ROOT / "oracle" / "_build"
 
 HOST_SRC = sorted((PKG / "csrc" / "host").glob("*.cpp"))
-CUDA_SRC = sorted((PKG / "csrc" / "cuda").glob("*.cu"))
+# numerics.cpp (quadrature, B-spline evaluation) is shared with the host
+# builder: device assembly tabulates its univariate tables with it
+CUDA_SRC = sorted((PKG / "csrc" / "cuda").glob("*.cu")) + [PKG / "csrc" / "host" / "numerics.cpp"]
 ORACLE_SRC = [ROOT / "oracle" / "oracle.cpp"]
 
 CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-shared", "-pthread", "-ffp-contract=off", "-Wall"]
@@ -28,6 +30,8 @@ NVCCFLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills",
+    # host code (numerics.cpp) rounds exactly as in libpmg_host
+    "-Xcompiler", "-ffp-contract=off",
     "-I" + str(ROOT / "include"),
 ]
 

@@ -140,6 +140,7 @@ struct pmg_ctx {
   std::vector<void*> allocs;
   size_t bytes = 0;
   long long launches = 0, spmv_launches = 0;
+  double assembly_seconds = 0.0;  // device stiffness assembly (PMG_BAND_ASSEMBLE levels)
   std::string err;
   // live event timing (pmg_profile)
   bool profiling = false;
@@ -354,6 +355,14 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
       ck(cudaMemcpy2DAsync(L.band + size_t(k) * L.Ob * Sp, sizeof(double) * Sp, hb.data(), sizeof(double) * S,
                            sizeof(double) * S, size_t(L.Ob), cudaMemcpyHostToDevice, c.stream),
          "band upload");
+    }
+  } else if (ld.band_format == PMG_BAND_ASSEMBLE) {
+    if (!D.geometry) throw PmgError(PMG_ERR_CONFIG, "device assembly needs the patch geometry (desc.geometry)");
+    try {
+      c.assembly_seconds +=
+          assemble_level_device(c.stream, d, p, ld.elements, D.geometry, c.pb, L.K, L.band, Sp, L.Ob);
+    } catch (const AssemblyError& e) {
+      throw PmgError(PMG_ERR_GEOMETRY, e.what());
     }
   } else {
     throw PmgError(PMG_ERR_CONFIG, "unknown band format");
@@ -1261,6 +1270,7 @@ int pmg_ctx_info(pmg_ctx* ctx, int what, int64_t* out) {
       case 2: *out = int64_t(ctx->bytes); break;
       case 3: *out = ctx->lv[level].N; break;
       case 4: *out = ctx->pe - ctx->pb; break;
+      case 5: *out = int64_t(ctx->assembly_seconds * 1e6); break;
       default: throw PmgError(PMG_ERR_CONFIG, "unknown info query");
     }
   });

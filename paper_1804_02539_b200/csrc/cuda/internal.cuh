@@ -17,8 +17,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <stdexcept>
 #include <string>
 #include <vector>
+
+#include "pmg_types.h"
 
 namespace pmgcu {
 
@@ -55,6 +58,17 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
+
+// ---------------------------------------------------------------- assembly
+// SingularGeometryError / bad geometry description of device assembly
+struct AssemblyError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+// Assemble the band of the K patches [patch_begin, patch_begin + K) of one
+// level into band ([K][Ob][Sp], rows < S; Ob offsets of the lower half or all
+// O).  Returns wall seconds (stream-synchronous).  assembly.cu.
+double assemble_level_device(cudaStream_t s, int dim, int degree, int elements, const pmg_patch_geometry* geo,
+                             int patch_begin, int K, double* band, long long Sp, int Ob);
 
 // ---------------------------------------------------------------- FD
 struct FdPiece {

@@ -21,6 +21,7 @@ struct pmgh_hierarchy {
   std::vector<double> rhs;
   pmgplan::RankPlan plan;  // last pmgh_rank_plan result
   std::vector<std::int32_t> nb_rank, nb_off, nb_iface;
+  std::vector<pmg_patch_geometry> geometry;  // empty if a patch map is not describable
 };
 
 namespace {
@@ -115,8 +116,8 @@ void fill_descriptors(pmgh_hierarchy* H) {
     d.elements = L.elements;
     d.num_dofs = L.mapper->num_dofs();
     d.l2g = L.l2g.data();
-    d.band_format = PMG_BAND_TENSOR;
-    d.band = L.band.data();
+    d.band_format = L.band.empty() ? PMG_BAND_ASSEMBLE : PMG_BAND_TENSOR;
+    d.band = L.band.empty() ? nullptr : L.band.data();
     if (l >= 1) {
       const TwoScaleMatrix& P = L.two_scale;
       d.ts_fine_dim = P.fine_dim;
@@ -160,6 +161,25 @@ void fill_descriptors(pmgh_hierarchy* H) {
     d.num_pieces = int(pv.size());
     d.pieces = pv.data();
   }
+  // patch geometry for device assembly: uniform open-knot spaces, free ends
+  H->geometry.clear();
+  for (const GeometryMap& g : h.domain().patches) {
+    pmg_patch_geometry pg;
+    std::memset(&pg, 0, sizeof pg);
+    bool ok = true;
+    for (int a = 0; a < g.dim(); ++a) {
+      const UnivariateSpace& sp = g.spaces()[a];
+      ok = ok && sp.left() == EndCondition::free_end && sp.right() == EndCondition::free_end;
+      pg.degree[a] = sp.degree();
+      pg.elements[a] = sp.elements();
+    }
+    pg.ctrl = g.control_points().data();
+    if (!ok) {
+      H->geometry.clear();
+      break;
+    }
+    H->geometry.push_back(pg);
+  }
   H->interfaces.clear();
   for (const auto& ifc : h.domain().interfaces) {
     H->interfaces.push_back(ifc.patch_a);
@@ -183,6 +203,11 @@ const char* pmgh_last_error(void) { return g_last_error.c_str(); }
 
 int pmgh_build(const char* domain, int split, int degree, int n0, int levels, const pmg_cycle_params* params,
                int rhs_kind, uint64_t seed, int threads, pmgh_hierarchy** out) {
+  return pmgh_build_ex(domain, split, degree, n0, levels, params, rhs_kind, seed, threads, 0, out);
+}
+
+int pmgh_build_ex(const char* domain, int split, int degree, int n0, int levels, const pmg_cycle_params* params,
+                  int rhs_kind, uint64_t seed, int threads, int flags, pmgh_hierarchy** out) {
   if (!out || !domain) return fail(PMG_ERR_CONFIG, "pmgh_build: null argument");
   *out = nullptr;
   return guarded([&] {
@@ -199,7 +224,9 @@ int pmgh_build(const char* domain, int split, int degree, int n0, int levels, co
       cp.damp_coarse = params->damp_coarse != 0;
     }
     RhsSpec rs = rhs_spec(H->domain, dom.dim, rhs_kind, seed);
-    H->h = std::make_unique<Hierarchy>(dom, degree, n0, levels, cp, rs, threads);
+    H->h = std::make_unique<Hierarchy>(dom, degree, n0, levels, cp, rs, threads,
+                                       (flags & PMGH_DEVICE_ASSEMBLY) == 0);
+    if ((flags & PMGH_DEVICE_ASSEMBLY) && dom.patches.empty()) throw ConfigError("pmgh_build: no patches");
     fill_descriptors(H.get());
     *out = H.release();
   });
@@ -223,6 +250,7 @@ int pmgh_describe(pmgh_hierarchy* H, pmg_hierarchy_desc* out) {
   out->coarse_n = h.coarse_matrix().rows;
   out->coarse_A = h.coarse_matrix().data();
   out->coarse_L = h.coarse_factor().data();
+  out->geometry = H->geometry.empty() ? nullptr : H->geometry.data();
   return PMG_OK;
 }
 

@@ -423,7 +423,7 @@ FDPayload make_fd(const std::vector<UnivariateSpace>& spaces, double sigma, doub
 }  // namespace
 
 Hierarchy::Hierarchy(const MultiPatchDomain& domain, int degree, int n0, int levels, CycleParams params,
-                     const RhsSpec& rhs, int threads)
+                     const RhsSpec& rhs, int threads, bool host_assembly)
     : domain_(std::make_unique<MultiPatchDomain>(domain)), degree_(degree), n0_(n0), params_(params) {
   if (levels < 1) throw ConfigError("hierarchy: need at least one refinement level");
   if (n0 < 1) throw ConfigError("hierarchy: coarsest element count must be positive");
@@ -485,6 +485,7 @@ Hierarchy::Hierarchy(const MultiPatchDomain& domain, int degree, int n0, int lev
   const int O = band_offsets(d, degree);
   for (int l = 0; l <= levels; ++l) {
     Level& L = levels_[l];
+    if (l >= 1 && !host_assembly) continue;  // assembled on the device
     const std::int64_t S = L.mapper->lattice_size();
     L.band.assign(std::size_t(S) * O * K, 0.0);
     // patches in parallel, element chunks inside a patch in parallel

@@ -77,8 +77,10 @@ struct RhsSpec {
 
 class Hierarchy {
  public:
+  // host_assembly = false leaves the bands of levels >= 1 empty: the device
+  // context assembles them from the patch geometry (PMG_BAND_ASSEMBLE)
   Hierarchy(const MultiPatchDomain& domain, int degree, int n0, int levels, CycleParams params,
-            const RhsSpec& rhs, int threads);
+            const RhsSpec& rhs, int threads, bool host_assembly = true);
   int dim() const { return domain_->dim; }
   int degree() const { return degree_; }
   int n0() const { return n0_; }

@@ -30,19 +30,28 @@ class CycleParams:
 
 
 class Hierarchy:
-    """Levels 0..levels with n0 * 2**l elements per patch direction."""
+    """Levels 0..levels with n0 * 2**l elements per patch direction.
+
+    assembly="device" leaves the stiffness of levels >= 1 unassembled on the
+    host: a GpuBackend context assembles it on the B200 from the patch
+    geometry (PMG_BAND_ASSEMBLE).  Such a hierarchy has no host band to give
+    the oracle; tests pair it with a host-assembled twin."""
 
     def __init__(self, domain: str, degree: int, levels: int, n0: int = 1, split: int = 1,
                  params: CycleParams | None = None, rhs: str = "default", seed: int = 42,
-                 threads: int | None = None):
+                 threads: int | None = None, assembly: str = "host"):
+        if assembly not in ("host", "device"):
+            raise ValueError("assembly must be 'host' or 'device'")
+        self.assembly = assembly
         lib = N.host_lib()
         self.params = params or CycleParams()
         self.domain = domain
         self.seed = seed
         self.threads = threads or os.cpu_count() or 1
         h = C.c_void_p()
-        rc = lib.pmgh_build(domain.encode(), split, degree, n0, levels, C.byref(self.params.to_c()),
-                            RHS_KINDS[rhs], seed, self.threads, C.byref(h))
+        flags = N.PMGH_DEVICE_ASSEMBLY if assembly == "device" else 0
+        rc = lib.pmgh_build_ex(domain.encode(), split, degree, n0, levels, C.byref(self.params.to_c()),
+                               RHS_KINDS[rhs], seed, self.threads, flags, C.byref(h))
         raise_for(rc, lib.pmgh_last_error().decode())
         self._h = h
         self.desc = N.PmgHierarchyDesc()
@@ -91,6 +100,8 @@ class Hierarchy:
         return np.ctypeslib.as_array(self.desc.levels[level].l2g, shape=(n,)).reshape(self.num_patches, -1)
 
     def band(self, level: int) -> np.ndarray:
+        if self.desc.levels[level].band_format != N.PMG_BAND_TENSOR:
+            raise ValueError(f"level {level} is assembled on the device; no host band")
         o = (2 * self.degree + 1) ** self.dim
         s = self.lattice_size(level)
         return np.ctypeslib.as_array(self.desc.levels[level].band, shape=(self.num_patches * o * s,)).reshape(

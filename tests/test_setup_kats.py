@@ -309,3 +309,28 @@ def test_gen_eig_cross_check_on_fd_payloads():
     assert np.abs(V.T @ M @ V - np.eye(m)).max() < 1e-10
     lam = np.diag(V.T @ K @ V)
     assert np.abs(np.sort(lam) - sla.eigh(K, M, eigvals_only=True)).max() < 1e-9 * lam.max()
+
+
+def test_device_assembly_descriptor():
+    """pmgh_build_ex(PMGH_DEVICE_ASSEMBLY): levels >= 1 carry no host band and
+    name PMG_BAND_ASSEMBLE; the patch geometry is described for the device;
+    host-only consumers refuse it loudly."""
+    from paper_1804_02539_b200 import _native as N
+    h = Hierarchy("c4", 3, 2, n0=2, assembly="device")
+    hh = Hierarchy("c4", 3, 2, n0=2)
+    assert h.desc.levels[0].band_format == N.PMG_BAND_TENSOR
+    for l in range(1, h.num_levels):
+        assert h.desc.levels[l].band_format == N.PMG_BAND_ASSEMBLE
+        assert not h.desc.levels[l].band
+        with pytest.raises(ValueError):
+            h.band(l)
+    assert np.array_equal(h.band(0), hh.band(0))
+    g = h.desc.geometry
+    assert g
+    for k in range(h.num_patches):
+        assert list(g[k].degree)[:3] == [1, 1, 1] and list(g[k].elements)[:3] == [1, 1, 1]
+        assert np.isfinite(g[k].ctrl[0])
+    import oracle
+    with pytest.raises(Exception):
+        oracle.Oracle(h)
+    assert h.assemble_seconds() < hh.assemble_seconds()
