@@ -557,9 +557,9 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   // kernels (many CTAs per piece) would not be faster
   const char* fsm = std::getenv("PMG_FD_SMALL_MAX");
   const long long small_max = fsm ? std::atoll(fsm) : 2048;
-  L.int_small = 2 * L.int_max_total + (long long)maxdim_int * maxdim_int <= kFdSmallDoubles &&
+  L.int_small = fd_small_smem(L.int_max_total, maxdim_int, d) <= kFdSmallDoubles * sizeof(double) &&
                 L.int_max_total <= small_max;
-  L.face_small = 2 * L.face_max_total + (long long)maxdim_face * maxdim_face <= kFdSmallDoubles &&
+  L.face_small = fd_small_smem(L.face_max_total, maxdim_face, 2) <= kFdSmallDoubles * sizeof(double) &&
                  L.face_max_total <= small_max;
   // pieces ordered so that equal (dims, factors) are adjacent
   auto piece_key = [&](const FdPiece& a) {
@@ -818,6 +818,42 @@ void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double
   const DevLevel& L = c.lv[l];
   const int d = c.dim;
   const int np = 2 * d;
+  // small levels on one rank: the whole smoother in one launch (interface
+  // totals summed from the replicas inside the kernel)
+  static const bool fused_ok = [] {
+    const char* e = std::getenv("PMG_NO_FUSED_SMOOTH");
+    return !(e && e[0] == '1');
+  }();
+  if (fused_ok && c.size == 1 && L.int_small && (L.n_face == 0 || L.face_small)) {
+    double flops = 0.0;
+    for (int pass = 0; pass < np; ++pass) flops += fd_pass_flops(L, L.int_dims, d, pass);
+    TimedScope ts(c, 1, l, flops);
+    SmoothSmallArgs a{};
+    a.d = d;
+    a.ints = L.d_int;
+    a.n_int = L.n_int;
+    a.faces = L.d_face;
+    a.n_face = L.n_face;
+    a.face_iface = L.face_iface;
+    a.edges = L.d_edges;
+    a.edge_items = L.edge_items;
+    a.n_edge_items = L.n_edge_items;
+    a.edge_iface = L.edge_iface;
+    a.vert_iface = L.vert_iface;
+    a.vert_scalar = L.vert_scalar;
+    a.nverts = L.n_verts;
+    a.rep_off = L.if_rep_off;
+    a.rep_slot = L.if_rep_slot;
+    a.r = r;
+    a.out = out;
+    a.add = add ? 1 : 0;
+    a.alpha = alpha;
+    const size_t smem = std::max(fd_small_smem(L.int_max_total, L.int_max_dim, d),
+                                 fd_small_smem(L.face_max_total, L.face_max_dim, 2));
+    launch_smooth_small(c.stream, a, smem);
+    c.launches++;
+    return;
+  }
   // interface pieces first, on the side stream when overlapping
   const cudaStream_t main = c.stream;
   const bool fork = c.overlap && !c.profiling && L.n_int > 0;

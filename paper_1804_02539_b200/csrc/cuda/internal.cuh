@@ -96,10 +96,11 @@ void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, in
 int fd_rows_per_block();
 int fd_pick_ntc(const long long* cols, const long long* weight, int n);
 void fd_configure();  // per device, before the first pass
-// whole solve of every piece in one launch, one CTA per piece, tensor and one
-// factor in shared memory: 2 max_total + max_dim^2 doubles <= kFdSmallDoubles
+// whole solve of every piece in one launch, one CTA per piece, tensor, diagonal
+// and every factor in shared memory: fd_small_smem(max_total, max_dim, naxes)
+// = 3 max_total + 2 naxes max_dim^2 doubles <= kFdSmallDoubles
 constexpr long long kFdSmallDoubles = 25000;
-size_t fd_small_smem(long long max_total, int max_dim);
+size_t fd_small_smem(long long max_total, int max_dim, int naxes);
 void launch_fd_small(cudaStream_t s, const FdPiece* pieces, int npieces, int naxes, long long max_total,
                      int max_dim, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
                      const double* work_in, double* work_out);
@@ -153,6 +154,29 @@ struct EdgePiece {
   long long dof_off;  // into the concatenated edge dof list
   const double* Linv; // column-major m x m
 };
+// one-launch smoother of a small level on one rank (kernels_fd.cu)
+struct SmoothSmallArgs {
+  int d;
+  const FdPiece* ints;
+  int n_int;
+  const FdPiece* faces;  // 3D face pieces; dofs at face_iface[work_off..]
+  int n_face;
+  const int* face_iface;
+  const EdgePiece* edges;
+  const int2* edge_items;
+  int n_edge_items;
+  const int* edge_iface;
+  const int* vert_iface;
+  const double* vert_scalar;
+  int nverts;
+  const int* rep_off;  // interface replica CSR
+  const int* rep_slot;
+  const double* r;
+  double* out;
+  int add;
+  double alpha;
+};
+void launch_smooth_small(cudaStream_t s, const SmoothSmallArgs& a, size_t smem);
 // items: (edge, first row) per CTA, 32 rows each.  Piece dofs are interface
 // indices: t holds their totals, rep_off/rep_slot their local replicas.
 void launch_edges_vertices(cudaStream_t s, const EdgePiece* edges, const int2* items, int nitems,

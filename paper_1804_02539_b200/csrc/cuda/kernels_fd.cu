@@ -23,6 +23,7 @@
 #include <cstdint>
 
 #include "internal.cuh"
+#include "pieces.cuh"
 
 namespace pmgcu {
 
@@ -209,6 +210,31 @@ __global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece*
   const long long lat_stride = naxes == 3 ? ext2 : ext;
   double* __restrict__ wout = work_out + P.work_off;
   const double* __restrict__ diag = P.diag;
+  // epilogues that read global data issue all their loads first, so the
+  // lane's 2 NTC reads are in flight together (one round trip, not 2 NTC)
+  if (out_mode == FD_OUT_WORK_DIAG || out_mode == FD_OUT_LATTICE_ADD) {
+    double ld[NTC][2];
+#pragma unroll
+    for (int j = 0; j < NTC; ++j)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int n = n0 + j * 8 + 2 * t + i;
+        const int nn = n < N ? n : N - 1;
+        ld[j][i] = out_mode == FD_OUT_WORK_DIAG ? diag[rl + R * nn] : lat_out[lat_row + lat_stride * nn];
+      }
+#pragma unroll
+    for (int j = 0; j < NTC; ++j)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int n = n0 + j * 8 + 2 * t + i;
+        if (n >= N) continue;
+        if (out_mode == FD_OUT_WORK_DIAG)
+          wout[rl + R * n] = acc[j][i] / ld[j][i];
+        else
+          lat_out[lat_row + lat_stride * n] = ld[j][i] + alpha * acc[j][i];
+      }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < NTC; ++j) {
 #pragma unroll
@@ -216,20 +242,10 @@ __global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece*
       const int n = n0 + j * 8 + 2 * t + i;
       if (n >= N) continue;
       const double v = acc[j][i];
-      const long long o = rl + R * n;
-      switch (out_mode) {
-        case FD_OUT_WORK:
-          wout[o] = v;
-          break;
-        case FD_OUT_WORK_DIAG:
-          wout[o] = v / diag[o];
-          break;
-        case FD_OUT_LATTICE_SET:
-          lat_out[lat_row + lat_stride * n] = alpha * v;
-          break;
-        default:
-          lat_out[lat_row + lat_stride * n] += alpha * v;
-      }
+      if (out_mode == FD_OUT_WORK)
+        wout[rl + R * n] = v;
+      else
+        lat_out[lat_row + lat_stride * n] = alpha * v;
     }
   }
 }
@@ -253,37 +269,108 @@ __device__ void small_axis(const double* __restrict__ in, double* __restrict__ o
   const int m = dims[axis];
   const int rows = inner * outer;
   const int tm_n = (rows + 7) / 8, tn_n = (m + 7) / 8, ks_n = (m + 3) / 4;
+  const int ntiles = tm_n * tn_n;
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
-  for (int tile = warp; tile < tm_n * tn_n; tile += nwarps) {
-    const int tm = tile % tm_n, tn = tile / tm_n;
-    const int r = tm * 8 + g;  // A row of this lane
-    const bool r_ok = r < rows;
-    const int rt = r_ok ? r % inner : 0, ro = r_ok ? r / inner : 0;
-    const double* arow = in + (long long)ro * inner * m + rt;
-    const int n = tn * 8 + g;  // B column of this lane
-    const bool n_ok = n < m;
-    double d0 = 0.0, d1 = 0.0;
+  // a warp runs two tiles' accumulator chains interleaved (DMMA latency)
+  for (int tile = warp; tile < ntiles; tile += 2 * nwarps) {
+    const int tiles[2] = {tile, tile + nwarps};
+    const double* arow[2];
+    bool r_ok[2], n_ok[2];
+    int n[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int tl = tiles[u] < ntiles ? tiles[u] : tile;
+      const int tm = tl % tm_n, tn = tl / tm_n;
+      const int r = tm * 8 + g;
+      r_ok[u] = r < rows && tiles[u] < ntiles;
+      const int rt = r < rows ? r % inner : 0, ro = r < rows ? r / inner : 0;
+      arow[u] = in + (long long)ro * inner * m + rt;
+      n[u] = tn * 8 + g;
+      n_ok[u] = n[u] < m && tiles[u] < ntiles;
+    }
+    double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     for (int ks = 0; ks < ks_n; ++ks) {
       const int k = ks * 4 + t4;
-      const double a = (r_ok && k < m) ? arow[(long long)k * inner] : 0.0;
-      const double b = (n_ok && k < m) ? Bs[k * m + n] : 0.0;
-      dmma(d0, d1, a, b);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const double a = (r_ok[u] && k < m) ? arow[u][(long long)k * inner] : 0.0;
+        const double b = (n_ok[u] && k < m) ? Bs[k * m + n[u]] : 0.0;
+        dmma(d[u][0], d[u][1], a, b);
+      }
     }
-    const int orow = tm * 8 + g;
-    if (orow < rows) {
-      const int ot = orow % inner, oo = orow / inner;
-      double* dst = out + (long long)oo * inner * m + ot;
-      const int j0 = tn * 8 + 2 * t4;
-      if (j0 < m) dst[(long long)j0 * inner] = d0;
-      if (j0 + 1 < m) dst[(long long)(j0 + 1) * inner] = d1;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (tiles[u] >= ntiles) continue;
+      const int tm = tiles[u] % tm_n, tn = tiles[u] / tm_n;
+      const int orow = tm * 8 + g;
+      if (orow < rows) {
+        const int ot = orow % inner, oo = orow / inner;
+        double* dst = out + (long long)oo * inner * m + ot;
+        const int j0 = tn * 8 + 2 * t4;
+        if (j0 < m) dst[(long long)j0 * inner] = d[u][0];
+        if (j0 + 1 < m) dst[(long long)(j0 + 1) * inner] = d[u][1];
+      }
     }
   }
 }
 
-__device__ void stage_matrix(double* Bs, const double* __restrict__ B, int m) {
-  for (int i = threadIdx.x; i < m * m; i += blockDim.x) Bs[i] = B[i];
+// The whole solve of one piece in one CTA.  Every factor (2 per axis) and the
+// diagonal are fetched with cp.async at entry, overlapping the input gather,
+// so the 2d products run back to back from shared memory.
+// smem: X, Y, diag (total each), then B[a][dir] (m_a^2 each).
+template <class In, class Out>
+__device__ void fd_small_body(const FdPiece& P, int naxes, In in, Out out, double* sm) {
+  const int dims[3] = {P.dims[0], P.dims[1], naxes == 3 ? P.dims[2] : 1};
+  const int total = int(P.total);
+  double* X = sm;
+  double* Y = sm + total;
+  double* D = sm + 2 * total;
+  double* Bs[3][2];
+  {
+    double* q = sm + 3 * total;
+    for (int a = 0; a < naxes; ++a)
+      for (int dir = 0; dir < 2; ++dir) {
+        Bs[a][dir] = q;
+        const int mm = dims[a] * dims[a];
+        const double* src = P.B[a][dir];
+        for (int i = threadIdx.x; i < mm; i += blockDim.x) cp_async8(q + i, src + i, true);
+        q += mm;
+      }
+    for (int i = threadIdx.x; i < total; i += blockDim.x) cp_async8(D + i, P.diag + i, true);
+    cp_async_commit();
+  }
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) X[idx] = in(idx);
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int a = 0; a < naxes; ++a) {  // w = (x_a V_a^T) r
+    small_axis(X, Y, Bs[a][0], naxes, dims, a);
+    __syncthreads();
+    double* tmp = X;
+    X = Y;
+    Y = tmp;
+  }
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) X[idx] = X[idx] / D[idx];
+  __syncthreads();
+  for (int a = 0; a < naxes; ++a) {  // x = (x_a V_a) w
+    small_axis(X, Y, Bs[a][1], naxes, dims, a);
+    __syncthreads();
+    double* tmp = X;
+    X = Y;
+    Y = tmp;
+  }
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) out(idx, X[idx]);
 }
+
+// lattice box of an interior piece: box index -> lattice slot
+struct LatticeBox {
+  long long base, ext, ext2;
+  int m0, m1;
+  __device__ __forceinline__ long long operator()(int idx) const {
+    const int i0 = idx % m0, i1 = (idx / m0) % m1, i2 = idx / (m0 * m1);
+    return base + i0 + ext * i1 + ext2 * i2;
+  }
+};
 
 __global__ void __launch_bounds__(kSmallThreads) fd_small_kernel(const FdPiece* __restrict__ pieces, int naxes,
                                                                  int in_mode, int out_mode,
@@ -292,77 +379,89 @@ __global__ void __launch_bounds__(kSmallThreads) fd_small_kernel(const FdPiece* 
                                                                  const double* __restrict__ work_in,
                                                                  double* __restrict__ work_out) {
   PMG_PDL_ENTRY();
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   const FdPiece& P = pieces[blockIdx.x];
-  const int dims[3] = {P.dims[0], P.dims[1], naxes == 3 ? P.dims[2] : 1};
-  const int total = int(P.total);
-  double* X = sm;
-  double* Y = sm + total;
-  double* Bs = sm + 2 * total;
-  const long long ext = P.ext, ext2 = (long long)P.ext * P.ext;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    double v;
-    if (in_mode == FD_IN_WORK) {
-      v = work_in[P.work_off + idx];
-    } else {
-      const int i0 = idx % dims[0], i1 = (idx / dims[0]) % dims[1], i2 = idx / (dims[0] * dims[1]);
-      v = lat_in[P.lat_base + i0 + ext * i1 + ext2 * i2];
-    }
-    X[idx] = v;
+  const LatticeBox box{P.lat_base, P.ext, (long long)P.ext * P.ext, P.dims[0], P.dims[1]};
+  const long long woff = P.work_off;
+  auto in = [&](int idx) { return in_mode == FD_IN_WORK ? work_in[woff + idx] : lat_in[box(idx)]; };
+  auto out = [&](int idx, double v) {
+    if (out_mode == FD_OUT_WORK || out_mode == FD_OUT_WORK_DIAG)
+      work_out[woff + idx] = v;
+    else if (out_mode == FD_OUT_LATTICE_SET)
+      lat_out[box(idx)] = alpha * v;
+    else
+      lat_out[box(idx)] += alpha * v;
+  };
+  fd_small_body(P, naxes, in, out, sm);
+}
+
+// The whole smoother of a small level on one rank, one launch
+// (HybridSmoother::apply, smoother.cpp:110-115): CTAs [0, n_int) solve the
+// interior pieces on the lattice; then the face pieces (3D), the edge items
+// and one vertex CTA act on interface totals that each CTA sums from the
+// replicas itself (the order iface_partial uses), and write every replica.
+// Pieces are disjoint, so the CTAs are independent.
+__global__ void __launch_bounds__(kSmallThreads) smooth_small_kernel(SmoothSmallArgs a) {
+  PMG_PDL_ENTRY();
+  extern __shared__ __align__(16) double sm[];
+  const ReplicaSum total{a.rep_off, a.rep_slot, a.r};
+  int b = blockIdx.x;
+  if (b < a.n_int) {
+    const FdPiece& P = a.ints[b];
+    const LatticeBox box{P.lat_base, P.ext, (long long)P.ext * P.ext, P.dims[0], P.dims[1]};
+    const double* __restrict__ r = a.r;
+    double* __restrict__ o = a.out;
+    const double alpha = a.alpha;
+    if (a.add)
+      fd_small_body(P, a.d, [&](int idx) { return r[box(idx)]; }, [&](int idx, double v) { o[box(idx)] += alpha * v; },
+                    sm);
+    else
+      fd_small_body(P, a.d, [&](int idx) { return r[box(idx)]; }, [&](int idx, double v) { o[box(idx)] = alpha * v; },
+                    sm);
+    return;
   }
-  __syncthreads();
-  for (int a = 0; a < naxes; ++a) {  // w = (x_a V_a^T) r
-    stage_matrix(Bs, P.B[a][0], dims[a]);
-    __syncthreads();
-    small_axis(X, Y, Bs, naxes, dims, a);
-    __syncthreads();
-    double* tmp = X;
-    X = Y;
-    Y = tmp;
+  b -= a.n_int;
+  if (b < a.n_face) {
+    const FdPiece& P = a.faces[b];
+    const int* __restrict__ g = a.face_iface + P.work_off;
+    fd_small_body(
+        P, 2, [&](int idx) { return total(g[idx]); },
+        [&](int idx, double v) { write_replicas(a.rep_off, a.rep_slot, g[idx], a.alpha * v, a.out, a.add); }, sm);
+    return;
   }
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) X[idx] = X[idx] / P.diag[idx];
-  __syncthreads();
-  for (int a = 0; a < naxes; ++a) {  // x = (x_a V_a) w
-    stage_matrix(Bs, P.B[a][1], dims[a]);
-    __syncthreads();
-    small_axis(X, Y, Bs, naxes, dims, a);
-    __syncthreads();
-    double* tmp = X;
-    X = Y;
-    Y = tmp;
+  b -= a.n_face;
+  if (b < a.n_edge_items) {
+    const int2 it = a.edge_items[b];
+    edge_item(a.edges[it.x], it.y, a.edge_iface, total, a.rep_off, a.rep_slot, a.out, a.add, a.alpha);
+    return;
   }
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const double v = X[idx];
-    if (out_mode == FD_OUT_WORK || out_mode == FD_OUT_WORK_DIAG) {
-      work_out[P.work_off + idx] = v;
-    } else {
-      const int i0 = idx % dims[0], i1 = (idx / dims[0]) % dims[1], i2 = idx / (dims[0] * dims[1]);
-      const long long lat = P.lat_base + i0 + ext * i1 + ext2 * i2;
-      if (out_mode == FD_OUT_LATTICE_SET)
-        lat_out[lat] = alpha * v;
-      else
-        lat_out[lat] += alpha * v;
-    }
-  }
+  vertex_block(a.vert_iface, a.vert_scalar, a.nverts, total, a.rep_off, a.rep_slot, a.out, a.add, a.alpha);
 }
 
 }  // namespace
 
-size_t fd_small_smem(long long max_total, int max_dim) {
-  return size_t(2 * max_total + (long long)max_dim * max_dim) * sizeof(double);
+size_t fd_small_smem(long long max_total, int max_dim, int naxes) {
+  return size_t(3 * max_total + 2LL * naxes * max_dim * max_dim) * sizeof(double);
 }
 
 void launch_fd_small(cudaStream_t s, const FdPiece* pieces, int npieces, int naxes, long long max_total,
                      int max_dim, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
                      const double* work_in, double* work_out) {
   if (npieces == 0) return;
-  const size_t smem = fd_small_smem(max_total, max_dim);
-  launch_k(fd_small_kernel, dim3(npieces), dim3(kSmallThreads), smem, s, pieces, naxes, in_mode, out_mode, lat_in, lat_out, alpha,
-                                                       work_in, work_out);
+  const size_t smem = fd_small_smem(max_total, max_dim, naxes);
+  launch_k(fd_small_kernel, dim3(npieces), dim3(kSmallThreads), smem, s, pieces, naxes, in_mode, out_mode, lat_in,
+           lat_out, alpha, work_in, work_out);
+}
+
+void launch_smooth_small(cudaStream_t s, const SmoothSmallArgs& a, size_t smem) {
+  const int grid = a.n_int + a.n_face + a.n_edge_items + (a.nverts > 0 ? 1 : 0);
+  if (grid == 0) return;
+  launch_k(smooth_small_kernel, dim3(grid), dim3(kSmallThreads), smem, s, a);
 }
 
 void fd_configure() {
   cudaFuncSetAttribute(fd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(smooth_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(fd_pass_dmma_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<5>::smem));
   cudaFuncSetAttribute(fd_pass_dmma_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<9>::smem));
   cudaFuncSetAttribute(fd_pass_dmma_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<11>::smem));

@@ -7,6 +7,7 @@
 #include <cstdlib>
 
 #include "internal.cuh"
+#include "pieces.cuh"
 
 namespace pmgcu {
 
@@ -123,11 +124,7 @@ __global__ void scatter_kernel(const int* __restrict__ dof_g, long long ndof, co
   }
 }
 
-// Edge pieces: z = L_T^-1 (sum of replica shares) with the explicit inverse of
-// the banded operator (BandedCholesky::solve, banded.cpp:61-77).  One CTA per
-// (edge, 32-row chunk): lane = row, the 8 warps split the columns, partial
-// sums meet in shared memory in a fixed order.  The trailing CTA handles every
-// vertex piece (smoother.cpp:36-38).
+// Edge and vertex pieces (bodies in pieces.cuh) on the interface totals t.
 __global__ void __launch_bounds__(kThreads) edges_vertices_kernel(
     const EdgePiece* __restrict__ edges, const int2* __restrict__ items, int nitems,
     const int* __restrict__ edge_iface, const int* __restrict__ vert_iface, const double* __restrict__ vert_scalar,
@@ -136,52 +133,12 @@ __global__ void __launch_bounds__(kThreads) edges_vertices_kernel(
   PMG_PDL_ENTRY();
   // t: interface totals (sum over every replica, all ranks); rep_off/rep_slot:
   // this rank's replicas of each interface dof
-  __shared__ double buf[512];
-  __shared__ double part[kThreads / 32][32];
   if (blockIdx.x < nitems) {
     const int2 it = items[blockIdx.x];
-    const EdgePiece e = edges[it.x];
-    const int* dofs = edge_iface + e.dof_off;
-    for (int i = threadIdx.x; i < e.m; i += kThreads) buf[i] = t[dofs[i]];
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i = it.y + lane;
-    const int per = (e.m + 7) / 8;
-    const int j0 = warp * per, j1 = min(e.m, j0 + per);
-    double z0 = 0.0, z1 = 0.0;
-    if (i < e.m) {
-      int j = j0;
-      for (; j + 1 < j1; j += 2) {
-        z0 = fma(e.Linv[(long long)j * e.m + i], buf[j], z0);
-        z1 = fma(e.Linv[(long long)(j + 1) * e.m + i], buf[j + 1], z1);
-      }
-      if (j < j1) z0 = fma(e.Linv[(long long)j * e.m + i], buf[j], z0);
-    }
-    part[warp][lane] = z0 + z1;
-    __syncthreads();
-    if (warp == 0 && i < e.m) {
-      double z = 0.0;
-      for (int w = 0; w < kThreads / 32; ++w) z += part[w][lane];
-      const int g = dofs[i];
-      for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) {
-        if (add)
-          out[rep_slot[q]] += alpha * z;
-        else
-          out[rep_slot[q]] = alpha * z;
-      }
-    }
+    edge_item(edges[it.x], it.y, edge_iface, TotalsArray{t}, rep_off, rep_slot, out, add, alpha);
     return;
   }
-  for (int v = threadIdx.x; v < nverts; v += kThreads) {
-    const int g = vert_iface[v];
-    const double z = t[g] / vert_scalar[v];
-    for (int q = rep_off[g]; q < rep_off[g + 1]; ++q) {
-      if (add)
-        out[rep_slot[q]] += alpha * z;
-      else
-        out[rep_slot[q]] = alpha * z;
-    }
-  }
+  vertex_block(vert_iface, vert_scalar, nverts, TotalsArray{t}, rep_off, rep_slot, out, add, alpha);
 }
 
 __global__ void lattice_from_global_kernel(const int* __restrict__ l2g, const unsigned char* __restrict__ owner,
