@@ -850,6 +850,10 @@ void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double
     a.alpha = alpha;
     const size_t smem = std::max(fd_small_smem(L.int_max_total, L.int_max_dim, d),
                                  fd_small_smem(L.face_max_total, L.face_max_dim, 2));
+    if (const char* dbg = std::getenv("PMG_DEBUG_SMOOTH")) {  // timing experiments only
+      if (dbg[0] == '1') a.n_edge_items = a.nverts = 0;
+      if (dbg[0] == '2') a.n_int = a.n_face = 0;
+    }
     launch_smooth_small(c.stream, a, smem);
     c.launches++;
     return;
