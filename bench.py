@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target length of the CPU sample")
+    ap.add_argument("--assembly", default="host", choices=["host", "device"],
+                    help="stiffness assembly of levels >= 1 (device: on the B200, DESIGN.md 3a; "
+                         "no CPU baseline then, the oracle needs host bands)")
     return ap.parse_args()
 
 
@@ -125,7 +128,8 @@ def build_hierarchy(args, threads=None):
     dom, p, n0, lv = CONFIGS[args.config]
     if args.levels is not None:
         lv = args.levels
-    return Hierarchy(dom, p, lv, n0=n0, seed=args.seed, threads=threads)
+    return Hierarchy(dom, p, lv, n0=n0, seed=args.seed, threads=threads,
+                     assembly=getattr(args, "assembly", "host"))
 
 
 def workload_config(args, h, extra=None):
@@ -351,7 +355,7 @@ def main():
                       "share_of_step": fd_ms.value / ms_prof if ms_prof else None},
     }
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.assembly == "host":
         cpu = cpu_baseline(args, h, args.cpu_seconds)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -360,7 +364,9 @@ def main():
         "data": "synthetic (seeded generator of the BASELINE config; see DESIGN.md)",
         "config": workload_config(args, h, {"parallelism": f"patch-partitioned dp{world}",
                                             "pcg_iterations": iters, "final_rel_residual": rel_res,
-                                            "tol_margin": 1e-8 / rel_res}),
+                                            "tol_margin": 1e-8 / rel_res, "assembly": args.assembly,
+                                            "setup_s": {"host_assembly": h.assemble_seconds(),
+                                                        "device_assembly": b.assembly_seconds()}}),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * ndofs, "d2h_bytes_per_step": 8 * ndofs,

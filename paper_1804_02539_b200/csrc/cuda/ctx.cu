@@ -663,6 +663,32 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
     L.ts.col_off = c.upload(col_off);
     L.ts.col_row = c.upload(col_row);
     L.ts.col_val = c.upload(col_val);
+    {  // tile spans (rows and columns of the two-scale matrix are monotone windows)
+      bool mono = true;
+      for (int i = 1; i < nf; ++i) mono = mono && ld.ts_row_start[i] >= ld.ts_row_start[i - 1];
+      int ps = 0, rs = 0;
+      for (int i0 = 0; i0 < nf && mono; i0 += 1) {
+        const int i1 = std::min(nf, i0 + kTileF);
+        int lo = INT32_MAX, hi = 0;
+        for (int i = i0; i < i1; ++i) {
+          lo = std::min(lo, ld.ts_row_start[i]);
+          hi = std::max(hi, ld.ts_row_start[i] + ld.ts_row_len[i]);
+        }
+        ps = std::max(ps, hi - lo);
+      }
+      for (int j0 = 0; j0 < ncd && mono; ++j0) {
+        const int j1 = std::min(ncd, j0 + kTileC);
+        int lo = INT32_MAX, hi = 0;
+        for (int j = j0; j < j1; ++j)
+          for (int q = col_off[j]; q < col_off[j + 1]; ++q) {
+            lo = std::min(lo, col_row[q]);
+            hi = std::max(hi, col_row[q] + 1);
+          }
+        rs = std::max(rs, hi - lo);
+      }
+      L.ts.pspan = mono ? ps : 0;
+      L.ts.rspan = mono ? rs : 0;
+    }
     if (nf != L.ext) throw PmgError(PMG_ERR_DOMAIN, "transfer: fine level must have twice the elements");
   }
   L.f = c.alloc<double>(size_t(L.lat_n));
@@ -939,12 +965,24 @@ void op_smooth_iface(pmg_ctx& c, int l, const double* r, double* out, bool add, 
 // one-pass tensor transfers for 2D and for small 3D lattices; large 3D
 // lattices keep the axis-by-axis passes (fewer redundant loads)
 bool fused_transfer(const pmg_ctx& c, const DevLevel& F) { return c.dim == 2 || F.S <= 40000; }
+bool tiled_transfers() {
+  static const bool on = [] {
+    const char* e = std::getenv("PMG_NO_TILED_TRANSFER");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
 
 // restriction level l -> l-1 on distributed shares; out coarse (dist)
 void op_restrict(pmg_ctx& c, int l, const double* r, double* out) {
   const DevLevel& F = c.lv[l];
   const DevLevel& C = c.lv[l - 1];
   TimedScope ts(c, 2, l, 0.0);
+  if (c.dim == 2 && F.ts.rspan > 0 && tiled_transfers()) {
+    launch_restrict_tile2d(c.stream, F.ts, F.K, F.ext, C.ext, r, out, C.l2g);
+    c.launches++;
+    return;
+  }
   if (fused_transfer(c, F)) {
     launch_restrict_fused(c.stream, F.ts, F.K, c.dim, F.ext, C.ext, r, out, C.l2g);
     c.launches++;
@@ -967,6 +1005,11 @@ void op_prolong_add(pmg_ctx& c, int l, const double* coarse, double coef, double
   const DevLevel& F = c.lv[l];
   const DevLevel& C = c.lv[l - 1];
   TimedScope ts(c, 2, l, 0.0);
+  if (c.dim == 2 && F.ts.pspan > 0 && tiled_transfers()) {
+    launch_prolong_tile2d(c.stream, F.ts, F.K, F.ext, C.ext, coarse, coef, u, F.l2g);
+    c.launches++;
+    return;
+  }
   if (fused_transfer(c, F)) {
     launch_prolong_fused(c.stream, F.ts, F.K, c.dim, F.ext, C.ext, coarse, coef, u, F.l2g);
     c.launches++;

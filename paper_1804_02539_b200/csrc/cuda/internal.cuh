@@ -219,7 +219,18 @@ struct TsDev {
   const int* col_off;    // transpose CSR: [coarse+1]
   const int* col_row;    // fine rows, ascending
   const double* col_val;
+  // tiled 2D transfers: widest coarse range of kTileF consecutive fine rows,
+  // widest fine range of kTileC consecutive coarse columns (0: not tileable)
+  int pspan = 0, rspan = 0;
 };
+constexpr int kTileF = 32;  // prolongation: fine tile kTileF x kTileF
+constexpr int kTileC = 16;  // restriction: coarse tile kTileC x kTileC
+// 2D transfers through a shared-memory tile (axis 0 then axis 1, the
+// reference's order per output); same results as the fused kernels
+void launch_restrict_tile2d(cudaStream_t s, const TsDev& ts, int K, int ext_f, int ext_c, const double* r,
+                            double* out, const int* l2g_c);
+void launch_prolong_tile2d(cudaStream_t s, const TsDev& ts, int K, int ext_f, int ext_c, const double* c, double coef,
+                           double* u, const int* l2g_f);
 // one tensor axis pass over K patches: in dims -> out dims (axis changes
 // extent).  mode 0 writes; 1 writes with Dirichlet slots zeroed (l2g of the
 // output lattice); 2 adds coef * value on non-Dirichlet slots.

@@ -396,6 +396,103 @@ __global__ void prolong_fused_kernel(TsDev ts, int K, int d, int ext_f, int ext_
   }
 }
 
+// 2D restriction of one coarse tile (kTileC x kTileC) per CTA: the fine
+// window it reads is staged in shared memory, axis 0 is contracted into a
+// second tile, then axis 1 -- per output the same sums in the same order as
+// restrict_fused_kernel (s0 over q0 inner, s1 over q1).
+__global__ void __launch_bounds__(kThreads) restrict_tile2d_kernel(TsDev ts, int K, int ext_f, int ext_c,
+                                                                   const double* __restrict__ r,
+                                                                   double* __restrict__ out,
+                                                                   const int* __restrict__ l2g_c) {
+  PMG_PDL_ENTRY();
+  extern __shared__ __align__(16) double tsm[];
+  const int tiles = (ext_c + kTileC - 1) / kTileC;
+  const int k = blockIdx.x / (tiles * tiles);
+  const int t = blockIdx.x % (tiles * tiles);
+  const int a0 = (t % tiles) * kTileC, a1 = (t / tiles) * kTileC;
+  const int b0 = min(ext_c, a0 + kTileC), b1 = min(ext_c, a1 + kTileC);
+  const int span = ts.rspan;
+  // fine windows of the tile's columns (monotone): first row of a, last of b-1
+  const int f0 = ts.col_row[ts.col_off[a0]], f1 = ts.col_row[ts.col_off[a1]];
+  const int n0 = ts.col_row[ts.col_off[b0] - 1] + 1 - f0, n1 = ts.col_row[ts.col_off[b1] - 1] + 1 - f1;
+  double* R = tsm;                   // [n1][span]
+  double* T = tsm + span * span;     // [n1][kTileC]
+  const double* __restrict__ src = r + (long long)k * ext_f * ext_f;
+  for (int idx = threadIdx.x; idx < n1 * n0; idx += blockDim.x) {
+    const int y = idx / n0, x = idx % n0;
+    R[y * span + x] = src[(long long)(f1 + y) * ext_f + f0 + x];
+  }
+  __syncthreads();
+  const int w0 = b0 - a0;
+  for (int idx = threadIdx.x; idx < n1 * w0; idx += blockDim.x) {
+    const int y = idx / w0, j0 = a0 + idx % w0;
+    double s0 = 0.0;
+    for (int q0 = ts.col_off[j0]; q0 < ts.col_off[j0 + 1]; ++q0)
+      s0 = fma(ts.col_val[q0], R[y * span + ts.col_row[q0] - f0], s0);
+    T[y * kTileC + (j0 - a0)] = s0;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < (b1 - a1) * w0; idx += blockDim.x) {
+    const int j1 = a1 + idx / w0, j0 = a0 + idx % w0;
+    const long long o = (long long)k * ext_c * ext_c + (long long)j1 * ext_c + j0;
+    if (l2g_c[o] < 0) {
+      out[o] = 0.0;
+      continue;
+    }
+    double s1 = 0.0;
+    for (int q1 = ts.col_off[j1]; q1 < ts.col_off[j1 + 1]; ++q1)
+      s1 = fma(ts.col_val[q1], T[(ts.col_row[q1] - f1) * kTileC + (j0 - a0)], s1);
+    out[o] = s1;
+  }
+}
+
+// 2D prolongation u += coef P c of one fine tile (kTileF x kTileF) per CTA:
+// the coarse window is staged in shared memory, axis 0 then axis 1, as
+// prolong_fused_kernel per output.
+__global__ void __launch_bounds__(kThreads) prolong_tile2d_kernel(TsDev ts, int K, int ext_f, int ext_c,
+                                                                  const double* __restrict__ c, double coef,
+                                                                  double* __restrict__ u,
+                                                                  const int* __restrict__ l2g_f) {
+  PMG_PDL_ENTRY();
+  extern __shared__ __align__(16) double tsm[];
+  const int tiles = (ext_f + kTileF - 1) / kTileF;
+  const int k = blockIdx.x / (tiles * tiles);
+  const int t = blockIdx.x % (tiles * tiles);
+  const int a0 = (t % tiles) * kTileF, a1 = (t / tiles) * kTileF;
+  const int b0 = min(ext_f, a0 + kTileF), b1 = min(ext_f, a1 + kTileF);
+  const int span = ts.pspan;
+  const int c0 = ts.row_start[a0], c1 = ts.row_start[a1];
+  const int n0 = min(span, ext_c - c0), n1 = min(span, ext_c - c1);
+  double* Cs = tsm;                // [n1][span]
+  double* T = tsm + span * span;   // [n1][kTileF]
+  const double* __restrict__ src = c + (long long)k * ext_c * ext_c;
+  for (int idx = threadIdx.x; idx < n1 * n0; idx += blockDim.x) {
+    const int y = idx / n0, x = idx % n0;
+    Cs[y * span + x] = src[(long long)(c1 + y) * ext_c + c0 + x];
+  }
+  __syncthreads();
+  const int w0 = b0 - a0;
+  for (int idx = threadIdx.x; idx < n1 * w0; idx += blockDim.x) {
+    const int y = idx / w0, i0 = a0 + idx % w0;
+    const double* v0 = ts.vals + ts.row_off[i0];
+    const int st = ts.row_start[i0] - c0;
+    double s0 = 0.0;
+    for (int q0 = 0; q0 < ts.row_len[i0]; ++q0) s0 = fma(v0[q0], Cs[y * span + st + q0], s0);
+    T[y * kTileF + (i0 - a0)] = s0;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < (b1 - a1) * w0; idx += blockDim.x) {
+    const int i1 = a1 + idx / w0, i0 = a0 + idx % w0;
+    const long long o = (long long)k * ext_f * ext_f + (long long)i1 * ext_f + i0;
+    if (l2g_f[o] < 0) continue;
+    const double* v1 = ts.vals + ts.row_off[i1];
+    const int st = ts.row_start[i1] - c1;
+    double s1 = 0.0;
+    for (int q1 = 0; q1 < ts.row_len[i1]; ++q1) s1 = fma(v1[q1], T[(st + q1) * kTileF + (i0 - a0)], s1);
+    u[o] += coef * s1;
+  }
+}
+
 __global__ void masked_axpy_kernel(const int* __restrict__ l2g, long long n, double c, const double* __restrict__ val,
                                    double* __restrict__ u) {
   PMG_PDL_ENTRY();
@@ -589,6 +686,20 @@ void launch_prolong_fused(cudaStream_t s, const TsDev& ts, int K, int d, int ext
   long long n = K;
   for (int a = 0; a < d; ++a) n *= ext_f;
   launch_k(prolong_fused_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, ts, K, d, ext_f, ext_c, c, coef, u, l2g_f);
+}
+void launch_restrict_tile2d(cudaStream_t s, const TsDev& ts, int K, int ext_f, int ext_c, const double* r,
+                            double* out, const int* l2g_c) {
+  const int tiles = (ext_c + kTileC - 1) / kTileC;
+  const size_t smem = sizeof(double) * (size_t(ts.rspan) * ts.rspan + size_t(ts.rspan) * kTileC);
+  launch_k(restrict_tile2d_kernel, dim3(unsigned(K * tiles * tiles)), dim3(kThreads), smem, s, ts, K, ext_f, ext_c, r,
+           out, l2g_c);
+}
+void launch_prolong_tile2d(cudaStream_t s, const TsDev& ts, int K, int ext_f, int ext_c, const double* c, double coef,
+                           double* u, const int* l2g_f) {
+  const int tiles = (ext_f + kTileF - 1) / kTileF;
+  const size_t smem = sizeof(double) * (size_t(ts.pspan) * ts.pspan + size_t(ts.pspan) * kTileF);
+  launch_k(prolong_tile2d_kernel, dim3(unsigned(K * tiles * tiles)), dim3(kThreads), smem, s, ts, K, ext_f, ext_c, c,
+           coef, u, l2g_f);
 }
 void launch_masked_axpy(cudaStream_t s, const int* l2g, long long n, double c, const double* val, double* u) {
   if (n > 0) launch_k(masked_axpy_kernel, dim3(grid_for(n)), dim3(kThreads), 0, s, l2g, n, c, val, u);
