@@ -21,6 +21,7 @@
 // thread's copy addresses are computed once per CTA.  Flops per application
 // = sum_pieces 4 prod(m_a) sum(m_a).
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.cuh"
 #include "pieces.cuh"
@@ -38,12 +39,14 @@ constexpr int kXPer = kBM * kBK / kFdThreads;  // 4 X copies per thread and stag
 
 // column panel of NTC n-tiles (8 columns each); B row stride = 4 mod 16
 // doubles so the 4 x 8 B-fragment reads of a half-warp hit distinct banks
-template <int NTC>
+template <int NTC, int WM>
 struct FdTile {
+  static constexpr int BM = kBM * WM;  // rows per CTA: 4 warps x 8 WM
+  static constexpr int XPer = BM * kBK / kFdThreads;
   static constexpr int BN = 8 * NTC;
   static constexpr int BS = (BN + 11) / 16 * 16 + 4;
   static constexpr int BPer = (kBK * BN + kFdThreads - 1) / kFdThreads;
-  static constexpr size_t smem = sizeof(double) * kStagesFd * (kBM * kXS + kBK * BS);
+  static constexpr size_t smem = sizeof(double) * kStagesFd * (BM * kXS + kBK * BS);
 };
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
@@ -62,149 +65,12 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// One pass over a group of pieces with the same dims and the same factor B
-// (pieces are independent; a group's rows are concatenated so the M
-// dimension has no per-piece padding).  item = (first piece of the group,
-// first row of the panel within the group, first column, rows of the group).
+// store of one 8-row fragment row set (see the kernel's epilogue comment)
 template <int NTC>
-__global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece* __restrict__ pieces,
-                                                                  const int4* __restrict__ items, int pass,
-                                                                  int naxes, int in_mode, int out_mode,
-                                                                  const double* __restrict__ lat_in,
-                                                                  double* __restrict__ lat_out, double alpha,
-                                                                  const double* __restrict__ work_in,
-                                                                  double* __restrict__ work_out) {
-  PMG_PDL_ENTRY();
-  using T = FdTile<NTC>;
-  extern __shared__ __align__(16) double fd_smem[];  // Xs[kStagesFd][kBM * kXS], Bs[kStagesFd][kBK * BS]
-  auto Xs = reinterpret_cast<double(*)[kBM * kXS]>(fd_smem);
-  auto Bs = reinterpret_cast<double(*)[kBK * T::BS]>(fd_smem + kStagesFd * kBM * kXS);
-  const int4 it = items[blockIdx.x];
-  const FdPiece& P0 = pieces[it.x];
-  const int axis = pass % naxes;
-  const int dir = pass / naxes;
-  const int K = P0.dims[axis];
-  const int N = K;
-  const long long R = P0.total / K;  // rows per piece
-  const long long rows = it.w;       // rows of the group
-  const long long r0 = it.y;
-  const int n0 = it.z;
-  const int m0 = P0.dims[0], m1 = P0.dims[1];
-  const long long ext = P0.ext, ext2 = (long long)P0.ext * P0.ext;
-  const double* __restrict__ B = P0.B[axis][dir];
-  const int tid = threadIdx.x;
-
-  // per-thread copy plan: X element (rr, kk) = (tid/16 + 8j, tid%16); B element
-  // (kk, nn) of idx = tid + 128j
-  const int xk = tid % kBK;
-  const double* xsrc[kXPer];
-  bool xrow_ok[kXPer];
-#pragma unroll
-  for (int j = 0; j < kXPer; ++j) {
-    const long long r = r0 + tid / kBK + 8 * j;
-    xrow_ok[j] = r < rows;
-    const long long rg = xrow_ok[j] ? r : 0;
-    const FdPiece& P = pieces[it.x + int(rg / R)];
-    const long long rr = rg % R;
-    if (in_mode == FD_IN_WORK)
-      xsrc[j] = work_in + P.work_off + rr * K + xk;
-    else
-      xsrc[j] = lat_in + P.lat_base + (naxes == 3 ? ext * (rr % m1) + ext2 * (rr / m1) : ext * rr) + xk;
-  }
-  int boff[T::BPer], bkk[T::BPer], bdst[T::BPer];
-  bool bn_ok[T::BPer];
-#pragma unroll
-  for (int j = 0; j < T::BPer; ++j) {
-    const int idx = tid + kFdThreads * j;
-    const int nn = idx % T::BN, kk = idx / T::BN;
-    bn_ok[j] = n0 + nn < N && kk < kBK;
-    bkk[j] = kk;
-    boff[j] = kk * N + n0 + nn;
-    bdst[j] = kk * T::BS + nn;
-  }
-  auto load = [&](int stage, int k0) {
-    double* xs = Xs[stage];
-    double* bs = Bs[stage];
-#pragma unroll
-    for (int j = 0; j < kXPer; ++j) {
-      const bool ok = xrow_ok[j] && k0 + xk < K;
-      cp_async8(xs + (tid / kBK + 8 * j) * kXS + xk, ok ? xsrc[j] + k0 : B, ok);
-    }
-#pragma unroll
-    for (int j = 0; j < T::BPer; ++j) {
-      if (bkk[j] >= kBK) continue;
-      const bool ok = bn_ok[j] && k0 + bkk[j] < K;
-      cp_async8(bs + bdst[j], ok ? B + boff[j] + (long long)k0 * N : B, ok);
-    }
-  };
-
-  // epilogues that read global data (the diagonal, or u for u += tau z) pull
-  // their lines into L2 now, so the reads after the main loop hit L2: per
-  // column, the panel's 32 rows are 256 contiguous bytes
-  if (out_mode == FD_OUT_WORK_DIAG || out_mode == FD_OUT_LATTICE_ADD) {
-    const long long rl0 = r0 % R;
-    const FdPiece& Pf = pieces[it.x + int(r0 / R)];
-    for (int idx = tid; idx < 2 * T::BN; idx += kFdThreads) {
-      const int n = n0 + idx / 2;
-      if (n >= N) continue;
-      const double* a;
-      if (out_mode == FD_OUT_WORK_DIAG) {
-        a = Pf.diag + rl0 + R * n;
-      } else {
-        const long long lr = naxes == 3 ? (rl0 % m0) + ext * (rl0 / m0) : rl0;
-        a = lat_out + Pf.lat_base + lr + (naxes == 3 ? ext2 : ext) * n;
-      }
-      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a + 16 * (idx & 1)));
-    }
-  }
-
-  const int warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t = lane & 3;
-  double acc[NTC][2];
-#pragma unroll
-  for (int j = 0; j < NTC; ++j) acc[j][0] = acc[j][1] = 0.0;
-
-  const int nst = (K + kBK - 1) / kBK;
-#pragma unroll
-  for (int s = 0; s < kStagesFd - 1; ++s) {
-    if (s < nst) load(s, s * kBK);
-    cp_async_commit();
-  }
-  for (int s = 0; s < nst; ++s) {
-    const int cur = s % kStagesFd;
-    cp_async_wait<kStagesFd - 2>();
-    __syncthreads();
-    {  // prefetch stage s + 2 into the slot freed at s - 1
-      const int nxt = s + kStagesFd - 1;
-      if (nxt < nst) load(nxt % kStagesFd, nxt * kBK);
-      cp_async_commit();
-    }
-    const double* xs = Xs[cur] + (warp * 8 + g) * kXS + t;
-    const double* bs = Bs[cur] + t * T::BS + g;
-    // fragments of k-step ks + 1 are read while k-step ks multiplies
-    double af[2], bf[2][NTC];
-    af[0] = xs[0];
-#pragma unroll
-    for (int j = 0; j < NTC; ++j) bf[0][j] = bs[j * 8];
-#pragma unroll
-    for (int ks = 0; ks < kBK / 4; ++ks) {
-      const int c = ks & 1;
-      if (ks + 1 < kBK / 4) {
-        af[c ^ 1] = xs[(ks + 1) * 4];
-#pragma unroll
-        for (int j = 0; j < NTC; ++j) bf[c ^ 1][j] = bs[(ks + 1) * 4 * T::BS + j * 8];
-      }
-#pragma unroll
-      for (int j = 0; j < NTC; ++j) dmma(acc[j][0], acc[j][1], af[c], bf[c][j]);
-    }
-  }
-
-  // epilogue: lane holds row r0+8w+g of the group, columns n0+8j+2t+{0,1};
-  // within its piece, Y(rl, n) at rl + R n
-  const long long r = r0 + warp * 8 + g;
-  if (r >= rows) return;
-  const FdPiece& P = pieces[it.x + int(r / R)];
-  const long long rl = r % R;
+__device__ __forceinline__ void fd_epilogue(const FdPiece& P, long long rl, const double (&acc)[NTC][2], int n0, int N,
+                                            int t, int naxes, int m0, long long ext, long long ext2, long long R,
+                                            int out_mode, double alpha, double* __restrict__ lat_out,
+                                            double* __restrict__ work_out) {
   long long lat_row = 0;
   if (out_mode >= FD_OUT_LATTICE_SET) lat_row = P.lat_base + (naxes == 3 ? (rl % m0) + ext * (rl / m0) : rl);
   const long long lat_stride = naxes == 3 ? ext2 : ext;
@@ -247,6 +113,161 @@ __global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece*
       else
         lat_out[lat_row + lat_stride * n] = alpha * v;
     }
+  }
+}
+
+// One pass over a group of pieces with the same dims and the same factor B
+// (pieces are independent; a group's rows are concatenated so the M
+// dimension has no per-piece padding).  item = (first piece of the group,
+// first row of the panel within the group, first column, rows of the group).
+template <int NTC, int WM>
+__global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece* __restrict__ pieces,
+                                                                  const int4* __restrict__ items, int pass,
+                                                                  int naxes, int in_mode, int out_mode,
+                                                                  const double* __restrict__ lat_in,
+                                                                  double* __restrict__ lat_out, double alpha,
+                                                                  const double* __restrict__ work_in,
+                                                                  double* __restrict__ work_out) {
+  PMG_PDL_ENTRY();
+  using T = FdTile<NTC, WM>;
+  extern __shared__ __align__(16) double fd_smem[];  // Xs[kStagesFd][BM * kXS], Bs[kStagesFd][kBK * BS]
+  auto Xs = reinterpret_cast<double(*)[T::BM * kXS]>(fd_smem);
+  auto Bs = reinterpret_cast<double(*)[kBK * T::BS]>(fd_smem + kStagesFd * T::BM * kXS);
+  const int4 it = items[blockIdx.x];
+  const FdPiece& P0 = pieces[it.x];
+  const int axis = pass % naxes;
+  const int dir = pass / naxes;
+  const int K = P0.dims[axis];
+  const int N = K;
+  const long long R = P0.total / K;  // rows per piece
+  const long long rows = it.w;       // rows of the group
+  const long long r0 = it.y;
+  const int n0 = it.z;
+  const int m0 = P0.dims[0], m1 = P0.dims[1];
+  const long long ext = P0.ext, ext2 = (long long)P0.ext * P0.ext;
+  const double* __restrict__ B = P0.B[axis][dir];
+  const int tid = threadIdx.x;
+
+  // per-thread copy plan: X element (rr, kk) = (tid/16 + 8j, tid%16); B element
+  // (kk, nn) of idx = tid + 128j
+  const int xk = tid % kBK;
+  const double* xsrc[T::XPer];
+  bool xrow_ok[T::XPer];
+#pragma unroll
+  for (int j = 0; j < T::XPer; ++j) {
+    const long long r = r0 + tid / kBK + 8 * j;
+    xrow_ok[j] = r < rows;
+    const long long rg = xrow_ok[j] ? r : 0;
+    const FdPiece& P = pieces[it.x + int(rg / R)];
+    const long long rr = rg % R;
+    if (in_mode == FD_IN_WORK)
+      xsrc[j] = work_in + P.work_off + rr * K + xk;
+    else
+      xsrc[j] = lat_in + P.lat_base + (naxes == 3 ? ext * (rr % m1) + ext2 * (rr / m1) : ext * rr) + xk;
+  }
+  int boff[T::BPer], bkk[T::BPer], bdst[T::BPer];
+  bool bn_ok[T::BPer];
+#pragma unroll
+  for (int j = 0; j < T::BPer; ++j) {
+    const int idx = tid + kFdThreads * j;
+    const int nn = idx % T::BN, kk = idx / T::BN;
+    bn_ok[j] = n0 + nn < N && kk < kBK;
+    bkk[j] = kk;
+    boff[j] = kk * N + n0 + nn;
+    bdst[j] = kk * T::BS + nn;
+  }
+  auto load = [&](int stage, int k0) {
+    double* xs = Xs[stage];
+    double* bs = Bs[stage];
+#pragma unroll
+    for (int j = 0; j < T::XPer; ++j) {
+      const bool ok = xrow_ok[j] && k0 + xk < K;
+      cp_async8(xs + (tid / kBK + 8 * j) * kXS + xk, ok ? xsrc[j] + k0 : B, ok);
+    }
+#pragma unroll
+    for (int j = 0; j < T::BPer; ++j) {
+      if (bkk[j] >= kBK) continue;
+      const bool ok = bn_ok[j] && k0 + bkk[j] < K;
+      cp_async8(bs + bdst[j], ok ? B + boff[j] + (long long)k0 * N : B, ok);
+    }
+  };
+
+  // epilogues that read global data (the diagonal, or u for u += tau z) pull
+  // their lines into L2 now, so the reads after the main loop hit L2: per
+  // column, the panel's 32 rows are 256 contiguous bytes
+  if (out_mode == FD_OUT_WORK_DIAG || out_mode == FD_OUT_LATTICE_ADD) {
+    const long long rl0 = r0 % R;
+    const FdPiece& Pf = pieces[it.x + int(r0 / R)];
+    for (int idx = tid; idx < 2 * T::BN; idx += kFdThreads) {
+      const int n = n0 + idx / 2;
+      if (n >= N) continue;
+      const double* a;
+      if (out_mode == FD_OUT_WORK_DIAG) {
+        a = Pf.diag + rl0 + R * n;
+      } else {
+        const long long lr = naxes == 3 ? (rl0 % m0) + ext * (rl0 / m0) : rl0;
+        a = lat_out + Pf.lat_base + lr + (naxes == 3 ? ext2 : ext) * n;
+      }
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a + 16 * (idx & 1)));
+    }
+  }
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[WM][NTC][2];
+#pragma unroll
+  for (int u = 0; u < WM; ++u)
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) acc[u][j][0] = acc[u][j][1] = 0.0;
+
+  const int nst = (K + kBK - 1) / kBK;
+#pragma unroll
+  for (int s = 0; s < kStagesFd - 1; ++s) {
+    if (s < nst) load(s, s * kBK);
+    cp_async_commit();
+  }
+  for (int s = 0; s < nst; ++s) {
+    const int cur = s % kStagesFd;
+    cp_async_wait<kStagesFd - 2>();
+    __syncthreads();
+    {  // prefetch stage s + 2 into the slot freed at s - 1
+      const int nxt = s + kStagesFd - 1;
+      if (nxt < nst) load(nxt % kStagesFd, nxt * kBK);
+      cp_async_commit();
+    }
+    // warp w owns rows 8 WM w .. 8 WM w + 8 WM - 1 of the panel
+    const double* xs = Xs[cur] + (warp * 8 * WM + g) * kXS + t;
+    const double* bs = Bs[cur] + t * T::BS + g;
+    // fragments of k-step ks + 1 are read while k-step ks multiplies
+    double af[2][WM], bf[2][NTC];
+#pragma unroll
+    for (int u = 0; u < WM; ++u) af[0][u] = xs[u * 8 * kXS];
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) bf[0][j] = bs[j * 8];
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      const int c = ks & 1;
+      if (ks + 1 < kBK / 4) {
+#pragma unroll
+        for (int u = 0; u < WM; ++u) af[c ^ 1][u] = xs[u * 8 * kXS + (ks + 1) * 4];
+#pragma unroll
+        for (int j = 0; j < NTC; ++j) bf[c ^ 1][j] = bs[(ks + 1) * 4 * T::BS + j * 8];
+      }
+#pragma unroll
+      for (int j = 0; j < NTC; ++j)
+#pragma unroll
+        for (int u = 0; u < WM; ++u) dmma(acc[u][j][0], acc[u][j][1], af[c][u], bf[c][j]);
+    }
+  }
+
+  // epilogue: lane holds rows r0 + 8 WM w + 8 u + g of the group, columns
+  // n0+8j+2t+{0,1}; within its piece, Y(rl, n) at rl + R n
+#pragma unroll
+  for (int u = 0; u < WM; ++u) {
+    const long long r = r0 + warp * 8 * WM + 8 * u + g;
+    if (r >= rows) break;
+    fd_epilogue<NTC>(pieces[it.x + int(r / R)], r % R, acc[u], n0, N, t, naxes, m0, ext, ext2, R, out_mode, alpha,
+                     lat_out, work_out);
   }
 }
 
@@ -462,12 +483,14 @@ void launch_smooth_small(cudaStream_t s, const SmoothSmallArgs& a, size_t smem) 
 void fd_configure() {
   cudaFuncSetAttribute(fd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(smooth_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(fd_pass_dmma_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<5>::smem));
-  cudaFuncSetAttribute(fd_pass_dmma_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<9>::smem));
-  cudaFuncSetAttribute(fd_pass_dmma_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<11>::smem));
+#define PMG_FD_ATTR(NT, W) \
+  cudaFuncSetAttribute(fd_pass_dmma_kernel<NT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<NT, W>::smem));
+  PMG_FD_ATTR(5, 1) PMG_FD_ATTR(9, 1) PMG_FD_ATTR(11, 1) PMG_FD_ATTR(5, 2) PMG_FD_ATTR(9, 2) PMG_FD_ATTR(11, 2)
+#undef PMG_FD_ATTR
 }
 
-int fd_rows_per_block() { return kBM; }
+int fd_wm();
+int fd_rows_per_block() { return kBM * fd_wm(); }
 
 int fd_pick_ntc(const long long* cols, const long long* weight, int n) {
   // the column-panel width (in n-tiles) with the least padding over the
@@ -491,18 +514,26 @@ int fd_pick_ntc(const long long* cols, const long long* weight, int n) {
   return best;
 }
 
+int fd_wm() {
+  static const int v = [] {
+    const char* e = std::getenv("PMG_FD_WM");
+    return e && e[0] == '2' ? 2 : 1;
+  }();
+  return v;
+}
+
 void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int ntc, int pass,
                     int naxes, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
                     const double* work_in, double* work_out) {
   if (nitems == 0) return;
-#define PMG_FD_CASE(NT)                                                                                          \
-  if (ntc == NT) {                                                                                               \
-    launch_k(fd_pass_dmma_kernel<NT>, dim3(nitems), dim3(kFdThreads), FdTile<NT>::smem, s, pieces, items, pass,  \
-             naxes, in_mode,                                                                                     \
-             out_mode, lat_in, lat_out, alpha, work_in, work_out);                                               \
-    return;                                                                                                      \
+  const int wm = fd_wm();
+#define PMG_FD_CASE(NT, W)                                                                                     \
+  if (ntc == NT && wm == W) {                                                                                  \
+    launch_k(fd_pass_dmma_kernel<NT, W>, dim3(nitems), dim3(kFdThreads), FdTile<NT, W>::smem, s, pieces, items, \
+             pass, naxes, in_mode, out_mode, lat_in, lat_out, alpha, work_in, work_out);                      \
+    return;                                                                                                    \
   }
-  PMG_FD_CASE(5) PMG_FD_CASE(9) PMG_FD_CASE(11)
+  PMG_FD_CASE(5, 1) PMG_FD_CASE(9, 1) PMG_FD_CASE(11, 1) PMG_FD_CASE(5, 2) PMG_FD_CASE(9, 2) PMG_FD_CASE(11, 2)
 #undef PMG_FD_CASE
 }
 
