@@ -341,9 +341,12 @@ def main():
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
         "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
-        "kernel": ("spmv_tma_half_kernel (index-free symmetric half-band SpMV / residual, TMA bulk-copy stream), "
-                   "finest level; bytes = half band 8(S+D)/2 + vectors (SURVEY.md 8(d)); mirrored half re-read "
-                   "from L2, so the kernel is L2-throughput bound (DESIGN.md)"),
+        "kernel": (("spmv_sweep2d_kernel (2D line sweep over the line-major symmetric half band: each band "
+                    "value read once from HBM and used as lower and mirrored upper entry from shared memory)"
+                    if h.dim == 2 else
+                    "spmv_tma_half_kernel (index-free symmetric half-band SpMV / residual, TMA bulk-copy stream; "
+                    "mirrored half re-read from L2, so the kernel is L2-throughput bound)")
+                   + ", finest level; bytes = half band 8(S+D)/2 + vectors (SURVEY.md 8(d)), DESIGN.md"),
         "launches": nl.value, "avg_ms": sp_ms.value / max(nl.value, 1),
         "bytes_per_launch": sp_bytes.value / max(nl.value, 1), "peak_source": hbm_src,
         "timing": "CUDA events around every finest-level launch in an instrumented replay of the same K steps "

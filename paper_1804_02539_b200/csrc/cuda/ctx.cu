@@ -122,6 +122,7 @@ struct pmg_ctx {
   double* coarse_x = nullptr;
   double* partial = nullptr;
   int partial_n = 0;
+  bool sweep = true;  // 2D line-sweep SpMV (PMG_SWEEP=0 at creation: the 256-row TMA kernel)
   double* scal = nullptr;     // device scalars
   double* h_scal = nullptr;   // pinned mirror
   double* staging = nullptr;  // device global-vector staging (finest num_dofs)
@@ -209,6 +210,16 @@ struct pmg_ctx {
     allocs.push_back(p);
     bytes += count * sizeof(T);
     return static_cast<T*>(p);
+  }
+  template <class T>
+  void release(T* p, size_t count) {
+    for (auto it = allocs.begin(); it != allocs.end(); ++it)
+      if (*it == static_cast<void*>(p)) {
+        cudaFree(p);
+        allocs.erase(it);
+        bytes -= count * sizeof(T);
+        return;
+      }
   }
   template <class T>
   T* upload(const T* h, size_t count) {
@@ -369,6 +380,18 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   }
   L.l2g = c.upload(l2g, size_t(L.lat_n));
   launch_zero_dirichlet_band(c.stream, d, p, L.ext, S, Sp, L.K, L.Ob, L.l2g, L.band);
+  {
+    const char* e = std::getenv("PMG_SWEEP");
+    c.sweep = !(e && e[0] == '0');
+  }
+  if (const long long lm = spmv_sweep_band_doubles(d, p, L.ext, S, L.K, L.Ob != L.O, c.sweep)) {
+    double* nb = c.alloc<double>(size_t(lm));
+    launch_sweep_relayout(c.stream, p, L.ext, S, L.K, Sp, L.band, nb);
+    ck(cudaGetLastError(), "sweep relayout");
+    ck(cudaStreamSynchronize(c.stream), "sweep relayout");
+    c.release(L.band, band_n);
+    L.band = nb;
+  }
 
   // ---- replicas: global owner patch over all patches; local replica CSR
   std::vector<int> owner_patch(size_t(L.N), -1);
@@ -746,7 +769,7 @@ void build_ctx(pmg_ctx& c, const pmg_hierarchy_desc& D) {
   long long maxlat = 0;
   for (auto& L : c.lv) maxlat = std::max(maxlat, L.lat_n);
   c.partial_n = dot_blocks(maxlat);
-  for (auto& L : c.lv) c.partial_n = std::max(c.partial_n, spmv_partials(c.dim, c.degree, L.S, L.K));
+  for (auto& L : c.lv) c.partial_n = std::max(c.partial_n, spmv_partials(c.dim, c.degree, L.S, L.K, L.Ob != L.O, c.sweep));
   c.partial = c.alloc<double>(size_t(c.partial_n));
   c.scal = c.alloc<double>(16);
   ck(cudaMemsetAsync(c.scal, 0, 16 * sizeof(double), c.stream), "memset");
@@ -801,7 +824,7 @@ void op_spmv(pmg_ctx& c, int l, const double* x, const double* f, double* y, dou
   if (L.Ob != L.O && (reinterpret_cast<uintptr_t>(x) & 15))
     throw PmgError(PMG_ERR_CONFIG, "half-band SpMV needs a 16-byte aligned x (TMA window)");
   TimedScope ts(c, 0, l, bytes);
-  SpmvArgs a{c.dim, c.degree, L.ext, L.S, L.K, L.band, x, f, y, dot_partial, L.Ob != L.O, L.Sp};
+  SpmvArgs a{c.dim, c.degree, L.ext, L.S, L.K, L.band, x, f, y, dot_partial, L.Ob != L.O, L.Sp, c.sweep};
   launch_spmv(c.stream, a);
   c.launches++;
   c.spmv_launches++;
@@ -1158,7 +1181,7 @@ int pcg_device(pmg_ctx& c, const double* f, double tol, int max_iter, double* u,
   // iteration front: Ap, alpha, u += alpha p, r -= alpha Ap, |r| -> host
   auto front = [&]() {
     op_spmv(c, Lf, p, nullptr, Ap, c.partial);  // Ap and the partials of Ap.p
-    launch_sum_partials(c.stream, c.partial, spmv_partials(c.dim, c.degree, F.S, F.K), s + 1);
+    launch_sum_partials(c.stream, c.partial, spmv_partials(c.dim, c.degree, F.S, F.K, F.Ob != F.O, c.sweep), s + 1);
     if (c.size > 1) {  // pAp over all ranks, ascending rank order
       c.comm->allgather(c.stream, s + 1, c.rank_buf, 1);
       launch_sum_ranks(c.stream, c.rank_buf, c.size, 1, s + 1);

@@ -117,6 +117,7 @@ struct SpmvArgs {
   double* dot_partial; // optional: per-block partial of sum y*x (nullptr: none)
   int half = 0;        // band holds the lower half only ([K][(O+1)/2][Sp])
   long long Sp = 0;    // band row stride per (patch, offset): spmv_row_stride
+  int sweep = 1;       // 2D half band: the line-sweep kernel where it applies
 };
 void launch_spmv(cudaStream_t s, const SpmvArgs& a);
 int spmv_blocks(long long rows);
@@ -129,7 +130,13 @@ bool spmv_tma_level(int dim, int degree, long long S);
 // allowed, else O
 int spmv_stored_offsets(int dim, int degree, long long S, bool allow_half);
 // number of dot partials one launch writes
-int spmv_partials(int dim, int degree, long long S, int K);
+int spmv_partials(int dim, int degree, long long S, int K, bool half, bool sweep);
+// 2D line-sweep levels keep the band line-major ([K][ext][Ob][tw], zero
+// padded): its size in doubles (0: the level is not swept), and the
+// conversion from the offset-major band
+long long spmv_sweep_band_doubles(int dim, int degree, int ext, long long S, int K, bool half, bool sweep);
+void launch_sweep_relayout(cudaStream_t s, int degree, int ext, long long S, int K, long long Sp, const double* src,
+                           double* dst);
 
 // ---------------------------------------------------------------- misc kernels
 void launch_fill(cudaStream_t s, double* x, long long n, double v);

@@ -12,6 +12,7 @@
 // reads 32 consecutive rows = 256 contiguous bytes (band is offset-major).
 // The row's sum runs over the offsets in the reference CSR column order
 // (axis 0 fastest).
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -489,6 +490,279 @@ __global__ void __launch_bounds__(kRowsTma + 32) spmv_tma_half_kernel(SpmvArgs a
   }
 }
 
+// ---------------------------------------------------------------- 2D line sweep
+// 2D half band, lattice lines of at most kSweepMaxExt rows.  These levels keep
+// the band line-major: [K][line L][Ob offsets][tw], each offset row of a line
+// holding its ext values at columns [PADL, PADL + ext) between zero pads
+// (sweep_relayout_kernel builds it from the offset-major band once, at
+// upload).  A CTA owns the output lines [L0, L1) of one patch and streams the
+// band one lattice line at a time, as p+1 chunks: chunk q holds the offsets
+// with d1 = q - p (2p+1 of them; p+1 with d0 <= 0 at d1 = 0), contiguous, so
+// one bulk copy (TMA) fills one stage of a ring guarded by mbarriers.  Every
+// band value is used twice from shared memory: as the lower entry A(r, r-s)
+// of its own row (against x of lines L-p..L, held in a register window), and
+// as the mirrored upper entry A(r-s, r) of the row r-s in line L-m, m = p-q
+// (the accumulators of the last p+1 lines stay in registers).  A row of line
+// L' therefore receives its terms in the reference's column order: chunks
+// 0..p of line L' (lower rows, then the centre row), then chunk p-m of line
+// L'+m for m = 1..p (mirrored rows).  The band crosses HBM and L2 once, plus
+// the p tail lines past L1 whose chunks q < p-(L-L1) a segment's last rows
+// need.  Mirrored reads of columns outside the line land in the zero pads
+// (in the band those pairs are wrapped and hold exact zeros as well).
+constexpr int kSweepMaxExt = 288;
+constexpr int kSweepMaxStages = 16;
+
+struct SweepCfg {
+  int segs, seglen;    // line segments per patch and their length
+  int stages, tw, nc;  // ring depth (chunks), offset-row width, consumer threads
+};
+
+// offset-major [K][Ob][Sp] -> line-major [K][ext][Ob][tw] with zero pads
+template <int P>
+__global__ void sweep_relayout_kernel(const double* __restrict__ src, double* __restrict__ dst, int ext, int K,
+                                      long long Sp, int tw) {
+  constexpr int W = 2 * P + 1;
+  constexpr int OB = P * W + P + 1;
+  constexpr int PADL = (P + 1) & ~1;
+  const long long n = (long long)K * ext * OB * tw;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int c = int(e % tw);
+    const long long t = e / tw;
+    const int o = int(t % OB);
+    const long long kl = t / OB;
+    const int L = int(kl % ext);
+    const long long k = kl / ext;
+    const int i = c - PADL;
+    dst[e] = (i >= 0 && i < ext) ? src[((size_t)k * OB + o) * Sp + (size_t)L * ext + i] : 0.0;
+  }
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Consumer side of the sweep: one thread per column i of the line.  The
+// register arrays are indexed by line modulo p+1 (acc[s], xw[s] belong to the
+// line L with L - L0 = s mod p+1), and the line loop is unrolled p+1 times
+// (line<PH>), so no value is moved between lines.  x and f reach shared
+// memory through per-thread cp.async copies issued p lines ahead (x ring of
+// p+2 lines, f ring of p+2 lines); one commit group per line.
+template <int P>
+struct SweepConsumer {
+  static constexpr int W = 2 * P + 1;
+  static constexpr int PADL = (P + 1) & ~1;
+  static constexpr int NX = P + 2;  // x ring lines
+  static constexpr int NF = P + 2;  // f ring lines
+  const double* smem;  // band ring [stages][W][tw]
+  double* xs;          // [NX][tw]
+  double* fs;          // [NF][nc]
+  uint64_t *full, *empty;
+  const double* __restrict__ xk;
+  const double* __restrict__ fk;
+  double* __restrict__ yk;
+  int i, ext, tw, stages, nc, L0, L1, Lend;
+  bool col;
+  int st, ph;      // band ring: stage of the next chunk and its phase parity
+  int xcur, fcur;  // ring slots of line L
+  double acc[P + 1];
+  double xw[P + 1][W];
+  double prod;
+
+  __device__ __forceinline__ void issue_x(int line, int slot) {
+    if (col && line < Lend) cp_async8(xs + slot * tw + PADL + i, xk + (size_t)line * ext + i);
+  }
+
+  template <int PH>
+  __device__ __forceinline__ void line(int L) {
+    // this thread's copies of x(L) and f(L-p) (the group of line L-p) are done
+    cp_async_wait<P - 1>();
+    if (L < Lend) {
+      // every consumer has stored x(L) and finished line L-1
+      asm volatile("bar.sync 1, %0;\n" ::"r"(nc) : "memory");
+      {
+        int sx = xcur + P;
+        sx -= sx >= NX ? NX : 0;
+        issue_x(L + P, sx);
+        if (col && fk && L < L1) cp_async8(fs + fcur * nc + i, fk + (size_t)L * ext + i);
+      }
+      cp_async_commit();
+      const double* xl = xs + xcur * tw + PADL + (col ? i : 0);  // threads past the line read column 0
+#pragma unroll
+      for (int j = 0; j < W; ++j) xw[PH][j] = xl[j - P];
+      const int nq = L < L1 ? P + 1 : P - (L - L1);
+#pragma unroll
+      for (int q = 0; q <= P; ++q) {
+        if (q < nq) {
+          mbar_wait(&full[st], ph);
+          if (col) {
+            const double* T = smem + (size_t)st * W * tw + PADL + i;
+            if (L < L1) {  // lower entries of the rows of line L, d1 = q - p (d0 <= 0 at d1 = 0)
+              constexpr int dummy = 0;
+              (void)dummy;
+              const int sl = (PH + 1 + q) % (P + 1);  // slot of line L - (p - q)
+#pragma unroll
+              for (int w = 0; w < (q < P ? W : P + 1); ++w) acc[PH] = fma(T[w * tw], xw[sl][w], acc[PH]);
+            }
+            // mirrored entries A(r - s, r), s = (m, d0), m = p - q: row r of line L, offset -s
+            const int m = P - q;
+            if (L - m >= L0 && L - m < L1) {
+              const int sa = (PH + 1 + q) % (P + 1);  // slot of line L - m
+#pragma unroll
+              for (int d0 = (m == 0 ? 1 : -P); d0 <= P; ++d0)
+                acc[sa] = fma(T[(P - d0) * tw + d0], xw[PH][d0 + P], acc[sa]);
+            }
+          }
+          __syncwarp();
+          if ((i & 31) == 0) mbar_arrive(&empty[st]);
+          if (++st == stages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    } else {
+      cp_async_commit();  // one group per line
+    }
+    constexpr int SW = (PH + 1) % (P + 1);  // slot of line L - p, complete now
+    const int Lw = L - P;
+    if (Lw >= L0 && col) {
+      int sf = fcur + 2;  // slot of f(L - p)
+      sf -= sf >= NF ? NF : 0;
+      const double y = fk ? fs[sf * nc + i] - acc[SW] : acc[SW];
+      yk[(size_t)Lw * ext + i] = y;
+      prod = fma(y, xw[SW][P], prod);
+    }
+    acc[SW] = 0.0;  // the accumulator of line L+1
+    xcur = xcur + 1 == NX ? 0 : xcur + 1;
+    fcur = fcur + 1 == NF ? 0 : fcur + 1;
+  }
+};
+
+template <int P>
+__global__ void __launch_bounds__(kSweepMaxExt + 32, 1) spmv_sweep2d_kernel(SpmvArgs a, SweepCfg g) {
+  PMG_PDL_ENTRY();
+  constexpr int W = 2 * P + 1;
+  constexpr int OB = P * W + P + 1;  // stored offsets: d1 = -p..-1 (all d0), d1 = 0 (d0 <= 0)
+  constexpr int PADL = (P + 1) & ~1;
+  using C = SweepConsumer<P>;
+  extern __shared__ __align__(128) double smem[];  // [stages][W][tw] band chunks, [NX][tw] x, [NF][nc] f
+  __shared__ __align__(8) uint64_t full[kSweepMaxStages], empty[kSweepMaxStages];
+  __shared__ double red[kSweepMaxExt / 32];
+
+  const int ext = a.ext;
+  const int nc = g.nc;
+  const int tw = g.tw;
+  const int stages = g.stages;
+  const int k = blockIdx.x / g.segs;
+  const int L0 = (blockIdx.x - k * g.segs) * g.seglen;
+  const int L1 = min(ext, L0 + g.seglen);
+  const int Lend = min(ext, L1 + P);  // streamed lines [L0, Lend)
+  const long long S = a.S;
+  double* xs = smem + (size_t)stages * W * tw;
+  double* fs = xs + C::NX * tw;
+  const int tid = threadIdx.x;
+
+  for (int q = tid; q < C::NX * tw; q += blockDim.x) xs[q] = 0.0;  // x pads
+  if (tid == 0) {
+    for (int st = 0; st < stages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], nc / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+
+  if (tid >= nc) {  // producer thread: one bulk copy per chunk
+    if (tid == nc) {
+      const double* base = a.band + (size_t)k * ext * OB * tw;
+      int st = 0, ph = 0, step = 0;
+      for (int L = L0; L < Lend; ++L) {
+        // tail lines past L1 carry only the chunks q < p - (L - L1)
+        const int nq = L < L1 ? P + 1 : P - (L - L1);
+        for (int q = 0; q < nq; ++q, ++step) {
+          if (step >= stages) mbar_wait(&empty[st], ph ^ 1);
+          const unsigned bytes = unsigned((q < P ? W : P + 1) * tw * sizeof(double));
+          mbar_expect_tx(&full[st], bytes);
+          tma_load_1d(smem + (size_t)st * W * tw, base + ((size_t)L * OB + q * W) * tw, bytes, &full[st]);
+          if (++st == stages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  C c;
+  c.smem = smem;
+  c.xs = xs;
+  c.fs = fs;
+  c.full = full;
+  c.empty = empty;
+  c.i = tid;
+  c.col = tid < ext;
+  c.xk = a.x + (size_t)k * S;
+  c.fk = a.f ? a.f + (size_t)k * S : nullptr;
+  c.yk = a.y + (size_t)k * S;
+  c.ext = ext;
+  c.tw = tw;
+  c.stages = stages;
+  c.nc = nc;
+  c.L0 = L0;
+  c.L1 = L1;
+  c.Lend = Lend;
+  c.st = 0;
+  c.ph = 0;
+  c.xcur = 0;
+  c.fcur = 0;
+  c.prod = 0.0;
+  // lines L0-m (slot p+1-m) straight from global memory; x(L0..L0+p-1) as p groups
+#pragma unroll
+  for (int m = 1; m <= P; ++m) {
+    const int line = L0 - m;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const int cc = tid + j - P;
+      c.xw[P + 1 - m][j] = (c.col && line >= 0 && cc >= 0 && cc < ext) ? __ldg(c.xk + (size_t)line * ext + cc) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < W; ++j) c.xw[0][j] = 0.0;
+#pragma unroll
+  for (int m = 0; m <= P; ++m) c.acc[m] = 0.0;
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    c.issue_x(L0 + j, j);
+    cp_async_commit();
+  }
+  for (int L = L0; L < L1 + P; L += P + 1) {
+    c.template line<0>(L);
+    if (L + 1 < L1 + P) c.template line<1 % (P + 1)>(L + 1);
+    if (P >= 2 && L + 2 < L1 + P) c.template line<2 % (P + 1)>(L + 2);
+    if (P >= 3 && L + 3 < L1 + P) c.template line<3 % (P + 1)>(L + 3);
+    if (P >= 4 && L + 4 < L1 + P) c.template line<4 % (P + 1)>(L + 4);
+  }
+  cp_async_wait<0>();
+  if (a.dot_partial) {
+    double prod = c.prod;
+    for (int o = 16; o > 0; o >>= 1) prod += __shfl_down_sync(0xffffffffu, prod, o);
+    if ((tid & 31) == 0) red[tid >> 5] = prod;
+    asm volatile("bar.sync 1, %0;\n" ::"r"(nc) : "memory");
+    if (tid == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < nc / 32; ++w) sum += red[w];
+      a.dot_partial[blockIdx.x] = sum;
+    }
+  }
+}
+
 template <int D, int P>
 void launch_tma(cudaStream_t s, const SpmvArgs& a) {
   constexpr int W = 2 * P + 1;
@@ -513,6 +787,71 @@ void launch_tma(cudaStream_t s, const SpmvArgs& a) {
 }
 
 }  // namespace
+
+static int sm_count() {
+  static const int v = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return v;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+// Line-sweep configuration of one 2D level: ring depth from the shared-memory
+// budget, then enough line segments per patch to fill every SM
+// (PMG_SWEEP=0 at context creation disables the sweep, PMG_SWEEP_MIN_EXT
+// raises its threshold).
+template <int P>
+bool sweep_cfg_p(int ext, int K, SweepCfg* g, size_t* smem) {
+  constexpr int W = 2 * P + 1;
+  constexpr int PADL = (P + 1) & ~1;
+  static const int min_ext = env_int("PMG_SWEEP_MIN_EXT", 128);  // shorter lines: latency-bound, the 256-row kernel wins
+  static const int budget = env_int("PMG_SWEEP_SMEM", 200 * 1024);
+  if (ext > kSweepMaxExt || ext < min_ext || ext < 2 * P + 2) return false;
+  g->nc = (ext + 31) / 32 * 32;
+  g->tw = (PADL + ext + P + 2) & ~1;
+  const size_t stage = size_t(W) * g->tw * sizeof(double);
+  const size_t xbytes = size_t(P + 2) * (g->tw + g->nc) * sizeof(double);  // x and f rings
+  const long long st = (budget - (long long)xbytes) / (long long)stage;
+  if (st < 2) return false;
+  g->stages = int(st < kSweepMaxStages ? st : kSweepMaxStages);
+  *smem = g->stages * stage + xbytes;
+  const int per_sm = std::max(1, int((227 * 1024) / (*smem + 2048)));
+  const int target = sm_count() * per_sm;
+  int segs = std::max(1, target / std::max(K, 1));
+  segs = std::min(segs, std::max(1, ext / std::max(2 * P, 8)));
+  g->seglen = (ext + segs - 1) / segs;
+  g->segs = (ext + g->seglen - 1) / g->seglen;
+  return true;
+}
+
+static bool sweep_cfg(int dim, int degree, int ext, long long S, int K, bool half, bool sweep, SweepCfg* g,
+                      size_t* smem) {
+  if (!sweep || dim != 2 || !half || !spmv_tma_level(dim, degree, S)) return false;
+  switch (degree) {
+    case 1: return sweep_cfg_p<1>(ext, K, g, smem);
+    case 2: return sweep_cfg_p<2>(ext, K, g, smem);
+    case 3: return sweep_cfg_p<3>(ext, K, g, smem);
+    case 4: return sweep_cfg_p<4>(ext, K, g, smem);
+    default: return false;
+  }
+}
+
+template <int P>
+void launch_sweep(cudaStream_t s, const SpmvArgs& a, const SweepCfg& g, size_t smem) {
+  static size_t configured = 0;  // per process; one device per context thread
+  if (smem > configured) {
+    cudaFuncSetAttribute(spmv_sweep2d_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured = smem;
+  }
+  launch_k(spmv_sweep2d_kernel<P>, dim3(unsigned(g.segs * a.K)), dim3(g.nc + 32), smem, s, a, g);
+}
 
 // Every level of a specialised degree streams its band with TMA: on small
 // levels the one-thread-per-row loop is latency-bound (each thread walks its
@@ -547,12 +886,53 @@ int spmv_stored_offsets(int dim, int degree, long long S, bool allow_half) {
 
 int spmv_blocks(long long rows) { return int((rows + kThreads - 1) / kThreads); }
 
-int spmv_partials(int dim, int degree, long long S, int K) {
+long long spmv_sweep_band_doubles(int dim, int degree, int ext, long long S, int K, bool half, bool sweep) {
+  SweepCfg g;
+  size_t smem;
+  if (!sweep_cfg(dim, degree, ext, S, K, half, sweep, &g, &smem)) return 0;
+  const int W = 2 * degree + 1;
+  return (long long)K * ext * (degree * W + degree + 1) * g.tw;
+}
+
+void launch_sweep_relayout(cudaStream_t s, int degree, int ext, long long S, int K, long long Sp, const double* src,
+                           double* dst) {
+  SweepCfg g;
+  size_t smem;
+  if (!sweep_cfg(2, degree, ext, S, K, true, true, &g, &smem)) return;
+  switch (degree) {
+    case 1: sweep_relayout_kernel<1><<<1184, 256, 0, s>>>(src, dst, ext, K, Sp, g.tw); break;
+    case 2: sweep_relayout_kernel<2><<<1184, 256, 0, s>>>(src, dst, ext, K, Sp, g.tw); break;
+    case 3: sweep_relayout_kernel<3><<<1184, 256, 0, s>>>(src, dst, ext, K, Sp, g.tw); break;
+    case 4: sweep_relayout_kernel<4><<<1184, 256, 0, s>>>(src, dst, ext, K, Sp, g.tw); break;
+  }
+}
+
+static int ext_of(int dim, long long S) {
+  if (dim != 2) return 0;
+  long long e = 1;
+  while (e * e < S) ++e;
+  return int(e);
+}
+
+int spmv_partials(int dim, int degree, long long S, int K, bool half, bool sweep) {
+  SweepCfg g;
+  size_t smem;
+  if (sweep_cfg(dim, degree, ext_of(dim, S), S, K, half, sweep, &g, &smem)) return g.segs * K;
   if (spmv_tma_level(dim, degree, S)) return int((S + kRowsTma - 1) / kRowsTma * K);
   return spmv_blocks(S * K);
 }
 
 void launch_spmv(cudaStream_t s, const SpmvArgs& a) {
+  SweepCfg g;
+  size_t smem;
+  if (sweep_cfg(a.dim, a.degree, a.ext, a.S, a.K, a.half != 0, a.sweep != 0, &g, &smem)) {
+    switch (a.degree) {
+      case 1: launch_sweep<1>(s, a, g, smem); return;
+      case 2: launch_sweep<2>(s, a, g, smem); return;
+      case 3: launch_sweep<3>(s, a, g, smem); return;
+      case 4: launch_sweep<4>(s, a, g, smem); return;
+    }
+  }
   if (spmv_tma_level(a.dim, a.degree, a.S)) {
 #define PMG_TMA_CASE(D, P) \
   if (a.dim == D && a.degree == P) { launch_tma<D, P>(s, a); return; }

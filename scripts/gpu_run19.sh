@@ -1,2 +1,7 @@
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:spmv_kernel -c 2 -o gpurun_out/prof_spmv_small_c2 python scripts/solve_once.py c2 1 > gpurun_out/ncu_small.log 2>&1
-echo "ncu rc=$?"
+# round-1 re-entry check: full GPU suite, smoke, c2 + c4 bench lines
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 1800 python -m pytest tests -m gpu -q --tb=short 2>&1 | grep -E "^E  |^FAILED|passed|failed" | head -20
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
+timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; tail -c 3000 gpurun_out/bench_c2.json
+timeout 900 python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; tail -c 3000 gpurun_out/bench_c4.json

@@ -1,14 +1,8 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -q --tb=short -x 2>&1 | grep -E "^E  |^FAILED|passed|failed" | head -5
-for cfg in c2 c4; do
-for tm in 0 1024; do
-PMG_TMA_MIN_ROWS=$tm timeout 600 python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${cfg}_$tm.json 2> gpurun_out/bench_${cfg}_$tm.err; echo "$cfg $tm rc=$?"
-done; done
-python - <<'PY'
-import json,glob
-for f in sorted(glob.glob('gpurun_out/bench_c*_*.json')):
-    d=json.loads(open(f).read().strip().splitlines()[-1]); r=d['roofline']
-    print(f, round(d['ms_per_step'],2), '%.4g'%d['value'], round(r['achieved']), round(r['avg_ms']*1000,1), round(r['spmv_share_of_step'],3), round(r['fd_finest']['achieved_tflops'],2))
-PY
-python scripts/solve_once.py c2 1 > gpurun_out/solve_once.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/launches_c2_warm.csv python scripts/solve_once.py c2 1 > gpurun_out/ncu_c2.log 2>&1
-python scripts/ncu_summary.py gpurun_out/launches_c2_warm.csv | head -14
+# line-sweep SpMV: parity, bench on/off, warm launch list
+timeout 900 python -m pytest tests/test_gpu_parity.py -q --tb=short -x -k "line_sweep or half_band" 2>&1 | grep -E "^E  |^FAILED|passed|failed|Error" | head -20
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c2_sweep.json 2> gpurun_out/bench_c2_sweep.err; tail -c 1500 gpurun_out/bench_c2_sweep.json | head -c 1400; echo
+PMG_SWEEP=0 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c2_nosweep.json 2>&1; python -c "import json;d=json.load(open('gpurun_out/bench_c2_nosweep.json'));print('nosweep ms',d['ms_per_step'])"
+python scripts/solve_once.py c2 2 > gpurun_out/solve_once.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/launches_c2_warm.csv python scripts/solve_once.py c2 2 > gpurun_out/ncu_c2.log 2>&1
+echo "ncu rc=$?"
+python scripts/ncu_summary.py gpurun_out/launches_c2_warm.csv | head -24

@@ -1,12 +1,5 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_cpp_dropin.py -q --tb=short -x 2>&1 | grep -E "^E  |^FAILED|passed|failed" | head -5
-timeout 600 python scripts/determinism.py 5 2>&1 | tail -2
-for cfg in c2 c4; do
-for ov in 0 1; do
-PMG_NO_OVERLAP=$ov timeout 600 python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${cfg}_ov$ov.json 2> gpurun_out/bench_${cfg}_ov$ov.err; echo "$cfg $ov rc=$?"
-done; done
-python - <<'PY'
-import json,glob
-for f in sorted(glob.glob('gpurun_out/bench_c*_ov*.json')):
-    d=json.loads(open(f).read().strip().splitlines()[-1]); r=d['roofline']
-    print(f, round(d['ms_per_step'],2), '%.4g'%d['value'], round(r['achieved']), round(r['avg_ms']*1000,1), round(r['spmv_share_of_step'],3), round(r['fd_finest']['achieved_tflops'],2))
-PY
+# line-sweep SpMV v2 (chunk stages): parity, per-level spmv on/off, bench
+timeout 900 python -m pytest tests/test_gpu_parity.py -q --tb=short -x -k "line_sweep" 2>&1 | grep -E "^E  |^FAILED|passed|failed|Error" | head -20
+echo "== sweep"; timeout 600 python scripts/breakdown.py c2 3 2>&1 | grep -E "spmv|wall"
+echo "== nosweep"; PMG_SWEEP=0 timeout 600 python scripts/breakdown.py c2 3 2>&1 | grep -E "spmv|wall"
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c2_sweep.json 2> gpurun_out/bench_c2_sweep.err; python -c "import json;d=json.load(open('gpurun_out/bench_c2_sweep.json'));print('sweep ms',d['ms_per_step'], d['roofline']['avg_ms'], d['roofline']['frac'])"

@@ -1,12 +1,4 @@
-timeout 1500 python -m pytest tests -m gpu -q --tb=short -x 2>&1 | grep -E "^E  |^FAILED|passed|failed" | head -5
-timeout 600 python scripts/determinism.py 5 2>&1 | tail -1
-for cfg in c2 c4; do
-for pd in 0 1; do
-PMG_NO_PDL=$pd timeout 600 python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${cfg}_pdl$pd.json 2> gpurun_out/bench_${cfg}_pdl$pd.err; echo "$cfg $pd rc=$?"
-done; done
-python - <<'PY'
-import json,glob
-for f in sorted(glob.glob('gpurun_out/bench_c*_pdl*.json')):
-    d=json.loads(open(f).read().strip().splitlines()[-1]); r=d['roofline']
-    print(f, round(d['ms_per_step'],2), '%.4g'%d['value'], round(r['achieved']), round(r['avg_ms']*1000,1), round(r['spmv_share_of_step'],3), round(r['fd_finest']['achieved_tflops'],2))
-PY
+python scripts/solve_once.py c2 1 > gpurun_out/solve_once.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:sweep2d -c 8 -o gpurun_out/prof_sweep_c2 python scripts/solve_once.py c2 1 > gpurun_out/ncu_sweep.log 2>&1; echo "rc=$?"
+ncu -i gpurun_out/prof_sweep_c2.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,launch__grid_size,dram__bytes_read.sum,smsp__average_warp_latency_issue_stalled_barrier,smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio > gpurun_out/sweep_raw.csv 2>&1
+head -20 gpurun_out/sweep_raw.csv

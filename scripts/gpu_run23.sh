@@ -1,14 +1,5 @@
-timeout 1500 python -m pytest tests/test_gpu_parity.py -q --tb=short -x 2>&1 | grep -E "^E  |^FAILED|passed|failed" | head -5
-timeout 600 python scripts/determinism.py 3 2>&1 | tail -1
-for cfg in c2 c4; do
-timeout 600 python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${cfg}.json 2> gpurun_out/bench_${cfg}.err; echo "$cfg rc=$?"
-done
-python - <<'PY'
-import json,glob
-for f in ['gpurun_out/bench_c2.json','gpurun_out/bench_c4.json']:
-    d=json.loads(open(f).read().strip().splitlines()[-1]); r=d['roofline']
-    print(f, round(d['ms_per_step'],2), '%.4g'%d['value'], round(r['achieved']), round(r['avg_ms']*1000,1), round(r['spmv_share_of_step'],3), round(r['fd_finest']['achieved_tflops'],2))
-PY
+timeout 900 python -m pytest tests/test_gpu_parity.py -q --tb=short -x -k "line_sweep or half_band or c2 or c1" 2>&1 | grep -E "^E  |^FAILED|passed|failed|Error" | head -20
+echo "== sweep"; timeout 600 python scripts/breakdown.py c2 3 2>&1 | grep -E "spmv|wall"
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c2_sweep.json 2> gpurun_out/bench_c2_sweep.err; python -c "import json;d=json.load(open('gpurun_out/bench_c2_sweep.json'));print('sweep ms',d['ms_per_step'], d['roofline']['avg_ms'], d['roofline']['frac'])"
 python scripts/solve_once.py c2 1 > gpurun_out/solve_once.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/launches_c2_warm.csv python scripts/solve_once.py c2 1 > gpurun_out/ncu_c2.log 2>&1
-python scripts/ncu_summary.py gpurun_out/launches_c2_warm.csv > gpurun_out/launches_c2_warm.txt; head -12 gpurun_out/launches_c2_warm.txt
+ncu --set full --clock-control none --import-source on -k regex:sweep2d -c 1 -o gpurun_out/prof_sweep_c2 python scripts/solve_once.py c2 1 > gpurun_out/ncu_sweep.log 2>&1; echo "rc=$?"

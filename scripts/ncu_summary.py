@@ -1,27 +1,25 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list."""
-import collections, csv, io, sys
+"""Summarise an ncu --csv launch list (gpu__time_duration.sum per launch) by
+kernel name: total device time, share, launches, average.
 
-def load(path):
-    lines = [l for l in open(path) if l.startswith('"')]
-    rows = list(csv.DictReader(io.StringIO("".join(lines))))
-    out = []
-    for r in rows:
-        if r.get("Metric Name") != "gpu__time_duration.sum":
-            continue
-        v = float(r["Metric Value"].replace(",", ""))
-        unit = r["Metric Unit"]
-        v = v / 1e3 if unit in ("ns", "nsecond") else (v * 1e3 if unit in ("ms", "msecond") else v)
-        name = r["Kernel Name"].split("(")[0].replace("(anonymous namespace)::", "").replace("pmgcu::", "")
-        out.append((name, v, r["Grid Size"]))
-    return out
+  python scripts/ncu_summary.py launches.csv
+"""
+import csv
+import sys
+from collections import defaultdict
 
-if __name__ == "__main__":
-    rows = load(sys.argv[1])
-    agg = collections.defaultdict(lambda: [0, 0.0])
-    for name, v, g in rows:
-        agg[name][0] += 1
-        agg[name][1] += v
-    tot = sum(v[1] for v in agg.values())
-    print(f"launches {len(rows)}  total device time {tot:.1f} us")
-    for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
-        print(f"{v[1]:10.1f} us {100 * v[1] / tot:5.1f}%  n={v[0]:5d}  avg={v[1] / v[0]:8.2f} us  {k}")
+rows = list(csv.DictReader(line for line in open(sys.argv[1]) if not line.startswith("==")))
+tot = defaultdict(float)
+cnt = defaultdict(int)
+for r in rows:
+    if r.get("Metric Name") != "gpu__time_duration.sum":
+        continue
+    v = float(r["Metric Value"].replace(",", ""))
+    unit = r.get("Metric Unit", "ns")
+    v *= {"ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1e-3)
+    name = r["Kernel Name"]
+    tot[name] += v
+    cnt[name] += 1
+T = sum(tot.values())
+print(f"launches {sum(cnt.values())}  total device time {T:.1f} us")
+for name, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+    print(f"{v:12.1f} us {100 * v / T:5.1f}%  n={cnt[name]:5d}  avg={v / cnt[name]:8.2f} us  {name[:60]}")

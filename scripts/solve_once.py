@@ -1,5 +1,10 @@
-"""One PCG solve of a BASELINE config on cuda:0 (for ncu launch lists)."""
+"""Build the hierarchy of a BASELINE config and run N device-resident PCG
+solves (graph-replayed), for ncu launch lists and captures.
+
+  python scripts/solve_once.py [config] [solves] [levels]
+"""
 import sys
+import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -13,8 +18,9 @@ levels = int(sys.argv[3]) if len(sys.argv) > 3 else None
 dom, p, n0, lv = CONFIGS[name]
 h = Hierarchy(dom, p, lv if levels is None else levels, n0=n0)
 b = GpuBackend(h)
-f = b.to_distributed_owner(h.finest_level, h.rhs())
-u = b.zero_acc(h.finest_level)
-for _ in range(solves):
-    u, rep = b.pcg_solve_device(f, u=u)
-print(name, "iterations", rep.iterations, "launches", b.kernel_launches())
+L = h.finest_level
+f = b.to_distributed_owner(L, h.rhs())
+for i in range(solves):
+    t = time.perf_counter()
+    u, rep = b.pcg_solve_device(f)
+    print(f"solve {i}: {rep.iterations} iterations, {1e3 * (time.perf_counter() - t):.2f} ms wall")

@@ -199,3 +199,40 @@ def test_half_band_matches_full_band(dom, p, lv, n0, monkeypatch):
     assert rel(out["0"][1], out["1"][1]) < 1e-14
     assert rel(out["0"][0], ref.apply_op(L, u)) < 1e-13
     assert rel(out["0"][1], ref.residual(L, f, u)) < 1e-13
+
+
+@pytest.mark.parametrize("dom,p,lv,n0", [("c1", 2, 5, 2), ("c1", 2, 6, 2), ("c2", 4, 5, 2), ("c2", 4, 6, 2),
+                                         ("c3", 1, 6, 2), ("c3", 3, 5, 2), ("c3", 3, 6, 2), ("lshape", 3, 5, 1),
+                                         ("two_squares_flipped_D", 4, 5, 1)])
+def test_line_sweep_matches_tma_half(dom, p, lv, n0, monkeypatch):
+    """2D line-sweep SpMV (default where it applies) against the 256-row TMA
+    half-band kernel (PMG_SWEEP=0) on every level: same offsets in the same
+    column order per row, so the products agree to rounding of the fused
+    multiply-adds; both against the oracle.  Covers odd line lengths (p odd),
+    several line segments per patch, and the dot partials of Ap.p (PCG)."""
+    h = Hierarchy(dom, p, lv, n0=n0)
+    out = {}
+    for sweep in ("1", "0"):
+        monkeypatch.setenv("PMG_SWEEP", sweep)
+        b = GpuBackend(h)
+        res = []
+        for level in range(h.num_levels):
+            u = rand(h.num_dofs(level), 31 + level)
+            f = rand(h.num_dofs(level), 71 + level)
+            res.append((b.gather_global(level, b.apply_op(level, b.to_accumulated(level, u))),
+                        b.gather_global(level, b.residual(level, b.to_distributed_owner(level, f),
+                                                          b.to_accumulated(level, u)))))
+        fL = h.rhs()
+        u_sol, rep = b.pcg_solve(fL)
+        out[sweep] = (res, u_sol, rep.iterations)
+        del b
+    ref = oracle.Oracle(h)
+    for level in range(h.num_levels):
+        u = rand(h.num_dofs(level), 31 + level)
+        f = rand(h.num_dofs(level), 71 + level)
+        for j in range(2):
+            assert rel(out["1"][0][level][j], out["0"][0][level][j]) < 1e-14, (level, j)
+        assert rel(out["1"][0][level][0], ref.apply_op(level, u)) < 1e-13
+        assert rel(out["1"][0][level][1], ref.residual(level, f, u)) < 1e-13
+    assert out["1"][2] == out["0"][2]
+    assert rel(out["1"][1], out["0"][1]) < 1e-10
