@@ -35,7 +35,6 @@ constexpr int kBM = 32;          // rows per CTA (4 warps x 8)
 constexpr int kBK = 16;          // k per shared-memory stage
 constexpr int kXS = kBK + 4;     // X row stride (doubles): conflict-free A fragments
 constexpr int kStagesFd = 3;
-constexpr int kXPer = kBM * kBK / kFdThreads;  // 4 X copies per thread and stage
 
 // column panel of NTC n-tiles (8 columns each); B row stride = 4 mod 16
 // doubles so the 4 x 8 B-fragment reads of a half-warp hit distinct banks
@@ -121,7 +120,7 @@ __device__ __forceinline__ void fd_epilogue(const FdPiece& P, long long rl, cons
 // dimension has no per-piece padding).  item = (first piece of the group,
 // first row of the panel within the group, first column, rows of the group).
 template <int NTC, int WM>
-__global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece* __restrict__ pieces,
+__global__ void __launch_bounds__(kFdThreads, WM == 1 ? 4 : 2) fd_pass_dmma_kernel(const FdPiece* __restrict__ pieces,
                                                                   const int4* __restrict__ items, int pass,
                                                                   int naxes, int in_mode, int out_mode,
                                                                   const double* __restrict__ lat_in,
@@ -244,8 +243,11 @@ __global__ void __launch_bounds__(kFdThreads) fd_pass_dmma_kernel(const FdPiece*
     for (int u = 0; u < WM; ++u) af[0][u] = xs[u * 8 * kXS];
 #pragma unroll
     for (int j = 0; j < NTC; ++j) bf[0][j] = bs[j * 8];
+    // k-steps of 4 that hold rows of B (the last stage of a pass is short)
+    const int nks = min(kBK / 4, (K - s * kBK + 3) / 4);
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
+      if (ks >= nks) break;
       const int c = ks & 1;
       if (ks + 1 < kBK / 4) {
 #pragma unroll

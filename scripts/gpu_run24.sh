@@ -1,2 +1,3 @@
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:fd_pass_dmma -s 0 -c 4 -o gpurun_out/prof_fd3_c2 python scripts/solve_once.py c2 1 > gpurun_out/ncu_fd3.log 2>&1
-echo "ncu rc=$?"
+timeout 900 python -m pytest tests/test_gpu_parity.py -q --tb=short -x -k "smooth and (c2 or c3 or c4)" 2>&1 | grep -E "^E  |^FAILED|passed|failed|Error" | head -20
+echo "== default"; timeout 600 python scripts/breakdown.py c2 3 2>&1 | grep -E "fd_interior|wall"
+echo "== ntc11"; PMG_FD_NTC=11 timeout 600 python scripts/breakdown.py c2 3 2>&1 | grep -E "fd_interior|wall"
