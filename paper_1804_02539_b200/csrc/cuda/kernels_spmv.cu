@@ -815,7 +815,7 @@ bool sweep_cfg_p(int ext, int K, SweepCfg* g, size_t* smem) {
   static const int budget = env_int("PMG_SWEEP_SMEM", 200 * 1024);
   if (ext > kSweepMaxExt || ext < min_ext || ext < 2 * P + 2) return false;
   g->nc = (ext + 31) / 32 * 32;
-  g->tw = (PADL + ext + P + 2) & ~1;
+  g->tw = (PADL + ext + P + 1) & ~1;  // columns PADL - p .. PADL + ext - 1 + p, even (16-byte rows)
   const size_t stage = size_t(W) * g->tw * sizeof(double);
   const size_t xbytes = size_t(P + 2) * (g->tw + g->nc) * sizeof(double);  // x and f rings
   const long long st = (budget - (long long)xbytes) / (long long)stage;

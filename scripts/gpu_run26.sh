@@ -1,6 +1,4 @@
-for rep in 1 2; do
-for v in "PMG_FD_GROUP=1" "PMG_FD_GROUP=0 PMG_FD_NTC=9" "PMG_FD_GROUP=1 PMG_FD_NTC=9" "PMG_NO_OVERLAP=1"; do
-env $v timeout 600 python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ab.json 2> gpurun_out/ab.err
-python -c "
-import json; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); print('$v', round(d['ms_per_step'],2), round(d['roofline']['fd_finest']['achieved_tflops'],2))"
-done; done
+timeout 1200 python -m pytest tests/test_gpu_parity.py -q --tb=short -x -k "smooth or cycle or pcg" 2>&1 | grep -E "^E  |^FAILED|passed|failed|Error" | head -20
+echo "== small 4608"; timeout 600 python scripts/breakdown.py c2 3 2>&1 | grep -E "fd_interior|interface_pieces|wall"
+echo "== small 2048"; PMG_FD_SMALL_MAX=2048 timeout 600 python scripts/breakdown.py c2 3 2>&1 | grep -E "fd_interior|interface|wall"
+echo "== c4"; timeout 600 python scripts/breakdown.py c4 2 2>&1 | grep -E "fd_interior|interface|wall"
