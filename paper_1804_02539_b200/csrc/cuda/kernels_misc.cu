@@ -6,6 +6,7 @@
 // (the property the reference gets from ascending-rank sums, parallel.hpp:26-30).
 #include <cstdlib>
 
+#include "transfer_ops.cuh"
 #include "internal.cuh"
 #include "pieces.cuh"
 
@@ -336,30 +337,8 @@ __global__ void restrict_fused_kernel(TsDev ts, int K, int d, int ext_f, int ext
   }
   const long long total = Sc * K;
   for (long long idx = blockIdx.x * (long long)kThreads + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * kThreads) {
-    if (l2g_c[idx] < 0) {
-      out[idx] = 0.0;
-      continue;
-    }
-    const long long k = idx / Sc;
-    const long long rem = idx - k * Sc;
-    const int j0 = int(rem % ext_c), j1 = int((rem / ext_c) % ext_c), j2 = d == 3 ? int(rem / ((long long)ext_c * ext_c)) : 0;
-    const double* src = r + k * Sf;
-    double s2 = 0.0;
-    const int q2a = d == 3 ? ts.col_off[j2] : 0, q2b = d == 3 ? ts.col_off[j2 + 1] : 1;
-    for (int q2 = q2a; q2 < q2b; ++q2) {
-      const long long b2 = d == 3 ? (long long)ts.col_row[q2] * ext_f * ext_f : 0;
-      double s1 = 0.0;
-      for (int q1 = ts.col_off[j1]; q1 < ts.col_off[j1 + 1]; ++q1) {
-        const double* row = src + b2 + (long long)ts.col_row[q1] * ext_f;
-        double s0 = 0.0;
-        for (int q0 = ts.col_off[j0]; q0 < ts.col_off[j0 + 1]; ++q0) s0 = fma(ts.col_val[q0], row[ts.col_row[q0]], s0);
-        s1 = fma(ts.col_val[q1], s0, s1);
-      }
-      s2 = d == 3 ? fma(ts.col_val[q2], s1, s2) : s1;
-    }
-    out[idx] = s2;
-  }
+       idx += (long long)gridDim.x * kThreads)
+    out[idx] = l2g_c[idx] < 0 ? 0.0 : restrict_out(ts, d, ext_f, ext_c, Sc, Sf, r, idx);
 }
 
 __global__ void prolong_fused_kernel(TsDev ts, int K, int d, int ext_f, int ext_c, const double* __restrict__ c,
@@ -372,28 +351,8 @@ __global__ void prolong_fused_kernel(TsDev ts, int K, int d, int ext_f, int ext_
   }
   const long long total = Sf * K;
   for (long long idx = blockIdx.x * (long long)kThreads + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * kThreads) {
-    if (l2g_f[idx] < 0) continue;
-    const long long k = idx / Sf;
-    const long long rem = idx - k * Sf;
-    const int i0 = int(rem % ext_f), i1 = int((rem / ext_f) % ext_f), i2 = d == 3 ? int(rem / ((long long)ext_f * ext_f)) : 0;
-    const double* src = c + k * Sc;
-    const int n2 = d == 3 ? ts.row_len[i2] : 1;
-    double s2 = 0.0;
-    for (int q2 = 0; q2 < n2; ++q2) {
-      const long long b2 = d == 3 ? (long long)(ts.row_start[i2] + q2) * ext_c * ext_c : 0;
-      double s1 = 0.0;
-      for (int q1 = 0; q1 < ts.row_len[i1]; ++q1) {
-        const double* row = src + b2 + (long long)(ts.row_start[i1] + q1) * ext_c + ts.row_start[i0];
-        const double* v0 = ts.vals + ts.row_off[i0];
-        double s0 = 0.0;
-        for (int q0 = 0; q0 < ts.row_len[i0]; ++q0) s0 = fma(v0[q0], row[q0], s0);
-        s1 = fma(ts.vals[ts.row_off[i1] + q1], s0, s1);
-      }
-      s2 = d == 3 ? fma(ts.vals[ts.row_off[i2] + q2], s1, s2) : s1;
-    }
-    u[idx] += coef * s2;
-  }
+       idx += (long long)gridDim.x * kThreads)
+    if (l2g_f[idx] >= 0) u[idx] += coef * prolong_out(ts, d, ext_f, ext_c, Sc, Sf, c, idx);
 }
 
 // 2D restriction of one coarse tile (kTileC x kTileC) per CTA: the fine

@@ -1,6 +1,7 @@
+# persistent coarse cycle: parity, timing on/off
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q --tb=short -x -k "cycle or pcg" 2>&1 | grep -E "^E  |^FAILED|passed|failed|Error" | head -20
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
 for cfg in c2 c4; do
-for v in "PMG_FD_GROUP=1" "PMG_FD_NTC=9" "PMG_FD_NTC=5"; do
-env $v timeout 600 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ab.json 2> gpurun_out/ab.err
-python -c "
-import json; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); print('$cfg $v', round(d['ms_per_step'],2), round(d['roofline']['fd_finest']['achieved_tflops'],2))"
-done; done
+echo "== $cfg cc"; timeout 600 python scripts/breakdown.py $cfg 3 2>&1 | grep -E "wall|coarse"
+echo "== $cfg no cc"; PMG_NO_COARSE_CYCLE=1 timeout 600 python scripts/breakdown.py $cfg 3 2>&1 | grep -E "wall"
+done

@@ -1,2 +1,2 @@
-timeout 1200 python -m pytest tests/test_gpu_assembly.py -q --tb=short -x 2>&1 | grep -E "^E  |^FAILED|passed|failed|Error" | head -10
-timeout 900 python scripts/assembly_bench.py c2 c4 2>&1 | tail -3 | tee gpurun_out/assembly_bench.txt
+PMG_COARSE_TRACE=1 timeout 300 python scripts/solve_once.py c2 2 2>&1 | tail -3
+PMG_COARSE_TRACE=1 timeout 300 python scripts/solve_once.py c4 1 2>&1 | tail -2
