@@ -122,7 +122,7 @@ struct pmg_ctx {
   double* coarse_x = nullptr;
   double* partial = nullptr;
   int partial_n = 0;
-  bool sweep = true;  // 2D line-sweep SpMV (PMG_SWEEP=0 at creation: the 256-row TMA kernel)
+  int sweep = 128;  // 2D line-sweep SpMV on lines of >= sweep rows; 0: off (PMG_SWEEP, PMG_SWEEP_MIN_EXT at creation)
   double* scal = nullptr;     // device scalars
   double* h_scal = nullptr;   // pinned mirror
   double* staging = nullptr;  // device global-vector staging (finest num_dofs)
@@ -382,7 +382,8 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   launch_zero_dirichlet_band(c.stream, d, p, L.ext, S, Sp, L.K, L.Ob, L.l2g, L.band);
   {
     const char* e = std::getenv("PMG_SWEEP");
-    c.sweep = !(e && e[0] == '0');
+    const char* m = std::getenv("PMG_SWEEP_MIN_EXT");
+    c.sweep = (e && e[0] == '0') ? 0 : std::max(1, m ? std::atoi(m) : 128);
   }
   if (const long long lm = spmv_sweep_band_doubles(d, p, L.ext, S, L.K, L.Ob != L.O, c.sweep)) {
     double* nb = c.alloc<double>(size_t(lm));

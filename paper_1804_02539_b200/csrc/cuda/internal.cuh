@@ -117,7 +117,7 @@ struct SpmvArgs {
   double* dot_partial; // optional: per-block partial of sum y*x (nullptr: none)
   int half = 0;        // band holds the lower half only ([K][(O+1)/2][Sp])
   long long Sp = 0;    // band row stride per (patch, offset): spmv_row_stride
-  int sweep = 1;       // 2D half band: the line-sweep kernel where it applies
+  int sweep = 128;     // 2D half band: line-sweep kernel on lines of >= sweep rows (0: off)
 };
 void launch_spmv(cudaStream_t s, const SpmvArgs& a);
 int spmv_blocks(long long rows);
@@ -130,11 +130,11 @@ bool spmv_tma_level(int dim, int degree, long long S);
 // allowed, else O
 int spmv_stored_offsets(int dim, int degree, long long S, bool allow_half);
 // number of dot partials one launch writes
-int spmv_partials(int dim, int degree, long long S, int K, bool half, bool sweep);
+int spmv_partials(int dim, int degree, long long S, int K, bool half, int sweep);
 // 2D line-sweep levels keep the band line-major ([K][ext][Ob][tw], zero
 // padded): its size in doubles (0: the level is not swept), and the
 // conversion from the offset-major band
-long long spmv_sweep_band_doubles(int dim, int degree, int ext, long long S, int K, bool half, bool sweep);
+long long spmv_sweep_band_doubles(int dim, int degree, int ext, long long S, int K, bool half, int sweep);
 void launch_sweep_relayout(cudaStream_t s, int degree, int ext, long long S, int K, long long Sp, const double* src,
                            double* dst);
 

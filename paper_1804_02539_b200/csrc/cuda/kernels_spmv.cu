@@ -805,13 +805,13 @@ static int env_int(const char* name, int dflt) {
 
 // Line-sweep configuration of one 2D level: ring depth from the shared-memory
 // budget, then enough line segments per patch to fill every SM
-// (PMG_SWEEP=0 at context creation disables the sweep, PMG_SWEEP_MIN_EXT
-// raises its threshold).
+// (min_ext: the shortest line swept, from the context: PMG_SWEEP=0 disables
+// the sweep, PMG_SWEEP_MIN_EXT sets the threshold, default 128 -- shorter
+// lines are latency-bound and the 256-row kernel is faster there).
 template <int P>
-bool sweep_cfg_p(int ext, int K, SweepCfg* g, size_t* smem) {
+bool sweep_cfg_p(int ext, int K, int min_ext, SweepCfg* g, size_t* smem) {
   constexpr int W = 2 * P + 1;
   constexpr int PADL = (P + 1) & ~1;
-  static const int min_ext = env_int("PMG_SWEEP_MIN_EXT", 128);  // shorter lines: latency-bound, the 256-row kernel wins
   static const int budget = env_int("PMG_SWEEP_SMEM", 200 * 1024);
   if (ext > kSweepMaxExt || ext < min_ext || ext < 2 * P + 2) return false;
   g->nc = (ext + 31) / 32 * 32;
@@ -831,14 +831,14 @@ bool sweep_cfg_p(int ext, int K, SweepCfg* g, size_t* smem) {
   return true;
 }
 
-static bool sweep_cfg(int dim, int degree, int ext, long long S, int K, bool half, bool sweep, SweepCfg* g,
+static bool sweep_cfg(int dim, int degree, int ext, long long S, int K, bool half, int sweep, SweepCfg* g,
                       size_t* smem) {
-  if (!sweep || dim != 2 || !half || !spmv_tma_level(dim, degree, S)) return false;
+  if (sweep <= 0 || dim != 2 || !half || !spmv_tma_level(dim, degree, S)) return false;
   switch (degree) {
-    case 1: return sweep_cfg_p<1>(ext, K, g, smem);
-    case 2: return sweep_cfg_p<2>(ext, K, g, smem);
-    case 3: return sweep_cfg_p<3>(ext, K, g, smem);
-    case 4: return sweep_cfg_p<4>(ext, K, g, smem);
+    case 1: return sweep_cfg_p<1>(ext, K, sweep, g, smem);
+    case 2: return sweep_cfg_p<2>(ext, K, sweep, g, smem);
+    case 3: return sweep_cfg_p<3>(ext, K, sweep, g, smem);
+    case 4: return sweep_cfg_p<4>(ext, K, sweep, g, smem);
     default: return false;
   }
 }
@@ -886,7 +886,7 @@ int spmv_stored_offsets(int dim, int degree, long long S, bool allow_half) {
 
 int spmv_blocks(long long rows) { return int((rows + kThreads - 1) / kThreads); }
 
-long long spmv_sweep_band_doubles(int dim, int degree, int ext, long long S, int K, bool half, bool sweep) {
+long long spmv_sweep_band_doubles(int dim, int degree, int ext, long long S, int K, bool half, int sweep) {
   SweepCfg g;
   size_t smem;
   if (!sweep_cfg(dim, degree, ext, S, K, half, sweep, &g, &smem)) return 0;
@@ -898,7 +898,7 @@ void launch_sweep_relayout(cudaStream_t s, int degree, int ext, long long S, int
                            double* dst) {
   SweepCfg g;
   size_t smem;
-  if (!sweep_cfg(2, degree, ext, S, K, true, true, &g, &smem)) return;
+  if (!sweep_cfg(2, degree, ext, S, K, true, 1, &g, &smem)) return;
   switch (degree) {
     case 1: sweep_relayout_kernel<1><<<1184, 256, 0, s>>>(src, dst, ext, K, Sp, g.tw); break;
     case 2: sweep_relayout_kernel<2><<<1184, 256, 0, s>>>(src, dst, ext, K, Sp, g.tw); break;
@@ -914,7 +914,7 @@ static int ext_of(int dim, long long S) {
   return int(e);
 }
 
-int spmv_partials(int dim, int degree, long long S, int K, bool half, bool sweep) {
+int spmv_partials(int dim, int degree, long long S, int K, bool half, int sweep) {
   SweepCfg g;
   size_t smem;
   if (sweep_cfg(dim, degree, ext_of(dim, S), S, K, half, sweep, &g, &smem)) return g.segs * K;
@@ -925,7 +925,7 @@ int spmv_partials(int dim, int degree, long long S, int K, bool half, bool sweep
 void launch_spmv(cudaStream_t s, const SpmvArgs& a) {
   SweepCfg g;
   size_t smem;
-  if (sweep_cfg(a.dim, a.degree, a.ext, a.S, a.K, a.half != 0, a.sweep != 0, &g, &smem)) {
+  if (sweep_cfg(a.dim, a.degree, a.ext, a.S, a.K, a.half != 0, a.sweep, &g, &smem)) {
     switch (a.degree) {
       case 1: launch_sweep<1>(s, a, g, smem); return;
       case 2: launch_sweep<2>(s, a, g, smem); return;

@@ -201,16 +201,22 @@ def test_half_band_matches_full_band(dom, p, lv, n0, monkeypatch):
     assert rel(out["0"][1], ref.residual(L, f, u)) < 1e-13
 
 
-@pytest.mark.parametrize("dom,p,lv,n0", [("c1", 2, 5, 2), ("c1", 2, 6, 2), ("c2", 4, 5, 2), ("c2", 4, 6, 2),
-                                         ("c3", 1, 6, 2), ("c3", 3, 5, 2), ("c3", 3, 6, 2), ("lshape", 3, 5, 1),
-                                         ("two_squares_flipped_D", 4, 5, 1)])
-def test_line_sweep_matches_tma_half(dom, p, lv, n0, monkeypatch):
-    """2D line-sweep SpMV (default where it applies) against the 256-row TMA
-    half-band kernel (PMG_SWEEP=0) on every level: same offsets in the same
-    column order per row, so the products agree to rounding of the fused
-    multiply-adds; both against the oracle.  Covers odd line lengths (p odd),
-    several line segments per patch, and the dot partials of Ap.p (PCG)."""
+@pytest.mark.parametrize("dom,p,lv,n0,min_ext", [
+    # PMG_SWEEP_MIN_EXT=1 sweeps every level with lines of >= 2p+2 rows:
+    # odd line lengths (p odd), one and several segments per patch, tails
+    ("c1", 2, 5, 2, "1"), ("c1", 2, 6, 2, "1"), ("c2", 4, 5, 2, "1"), ("c2", 4, 6, 2, "1"),
+    ("c3", 1, 6, 2, "1"), ("c3", 3, 5, 2, "1"), ("c3", 3, 6, 2, "1"), ("lshape", 3, 5, 1, "1"),
+    ("two_squares_flipped_D", 4, 5, 1, "1"),
+    # the default threshold (lines of >= 128 rows): the levels the bench sweeps
+    ("c1", 2, 7, 2, "128"), ("c3", 3, 7, 2, "128"), ("c2", 4, 7, 2, "128")])
+def test_line_sweep_matches_tma_half(dom, p, lv, n0, min_ext, monkeypatch):
+    """2D line-sweep SpMV against the 256-row TMA half-band kernel
+    (PMG_SWEEP=0) on every level: same offsets in the same column order per
+    row, so the products agree to rounding of the fused multiply-adds; both
+    against the oracle.  Covers odd line lengths (p odd), several line
+    segments per patch, and the dot partials of Ap.p (PCG)."""
     h = Hierarchy(dom, p, lv, n0=n0)
+    monkeypatch.setenv("PMG_SWEEP_MIN_EXT", min_ext)
     out = {}
     for sweep in ("1", "0"):
         monkeypatch.setenv("PMG_SWEEP", sweep)
