@@ -48,6 +48,8 @@ struct DevLevel {
   int Ob = 0;  // stored offsets per patch: O, or (O+1)/2 for the symmetric half band
   long long S = 0, Sp = 0, lat_n = 0, N = 0;
   double* band = nullptr;
+  double* sweep_scratch = nullptr;  // line sweep: segment-boundary rows
+  unsigned* sweep_flags = nullptr;
   int* l2g = nullptr;
   unsigned char* owner = nullptr;
   int* rep_off = nullptr;
@@ -392,6 +394,15 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
     ck(cudaStreamSynchronize(c.stream), "sweep relayout");
     c.release(L.band, band_n);
     L.band = nb;
+  }
+  {
+    long long nd = 0, nf = 0;
+    spmv_sweep_scratch(d, p, L.ext, S, L.K, L.Ob != L.O, c.sweep, &nd, &nf);
+    if (nf > 0) {
+      L.sweep_scratch = c.alloc<double>(size_t(nd));
+      L.sweep_flags = c.alloc<unsigned>(size_t(nf));
+      ck(cudaMemsetAsync(L.sweep_flags, 0, sizeof(unsigned) * nf, c.stream), "memset");
+    }
   }
 
   // ---- replicas: global owner patch over all patches; local replica CSR
@@ -825,7 +836,8 @@ void op_spmv(pmg_ctx& c, int l, const double* x, const double* f, double* y, dou
   if (L.Ob != L.O && (reinterpret_cast<uintptr_t>(x) & 15))
     throw PmgError(PMG_ERR_CONFIG, "half-band SpMV needs a 16-byte aligned x (TMA window)");
   TimedScope ts(c, 0, l, bytes);
-  SpmvArgs a{c.dim, c.degree, L.ext, L.S, L.K, L.band, x, f, y, dot_partial, L.Ob != L.O, L.Sp, c.sweep};
+  SpmvArgs a{c.dim, c.degree, L.ext, L.S, L.K, L.band, x, f, y, dot_partial, L.Ob != L.O, L.Sp, c.sweep,
+             L.sweep_scratch, L.sweep_flags};
   launch_spmv(c.stream, a);
   c.launches++;
   c.spmv_launches++;

@@ -118,6 +118,8 @@ struct SpmvArgs {
   int half = 0;        // band holds the lower half only ([K][(O+1)/2][Sp])
   long long Sp = 0;    // band row stride per (patch, offset): spmv_row_stride
   int sweep = 128;     // 2D half band: line-sweep kernel on lines of >= sweep rows (0: off)
+  double* sweep_scratch = nullptr;  // sweep: per segment boundary, the carry rows (spmv_sweep_scratch)
+  unsigned* sweep_flags = nullptr;  // sweep: per segment boundary, carry published (zeroed; reset by the reader)
 };
 void launch_spmv(cudaStream_t s, const SpmvArgs& a);
 int spmv_blocks(long long rows);
@@ -135,6 +137,8 @@ int spmv_partials(int dim, int degree, long long S, int K, bool half, int sweep)
 // padded): its size in doubles (0: the level is not swept), and the
 // conversion from the offset-major band
 long long spmv_sweep_band_doubles(int dim, int degree, int ext, long long S, int K, bool half, int sweep);
+void spmv_sweep_scratch(int dim, int degree, int ext, long long S, int K, bool half, int sweep, long long* doubles,
+                        long long* flags);
 void launch_sweep_relayout(cudaStream_t s, int degree, int ext, long long S, int K, long long Sp, const double* src,
                            double* dst);
 

@@ -505,10 +505,15 @@ __global__ void __launch_bounds__(kRowsTma + 32) spmv_tma_half_kernel(SpmvArgs a
 // (the accumulators of the last p+1 lines stay in registers).  A row of line
 // L' therefore receives its terms in the reference's column order: chunks
 // 0..p of line L' (lower rows, then the centre row), then chunk p-m of line
-// L'+m for m = 1..p (mirrored rows).  The band crosses HBM and L2 once, plus
-// the p tail lines past L1 whose chunks q < p-(L-L1) a segment's last rows
-// need.  Mirrored reads of columns outside the line land in the zero pads
-// (in the band those pairs are wrapped and hold exact zeros as well).
+// L'+m for m = 1..p (mirrored rows).  Every band line crosses HBM and L2
+// once.  Segment boundaries: the mirrored terms a segment's first p lines
+// give to rows of the previous segment's last p lines ("carry", summed in the
+// same line order) go to a scratch row per boundary, published early (after
+// line L0+p-1) with a release flag; the previous segment's CTA waits for the
+// flag when it reaches its end, which in practice has long been set, and adds
+// the carry: y = f - (partial + carry).  Mirrored reads of columns outside the
+// line land in the zero pads (in the band those pairs are wrapped and hold
+// exact zeros as well).
 constexpr int kSweepMaxExt = 288;
 constexpr int kSweepMaxStages = 16;
 
@@ -535,6 +540,15 @@ __global__ void sweep_relayout_kernel(const double* __restrict__ src, double* __
     const int i = c - PADL;
     dst[e] = (i >= 0 && i < ext) ? src[((size_t)k * OB + o) * Sp + (size_t)L * ext + i] : 0.0;
   }
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -567,6 +581,11 @@ struct SweepConsumer {
   double* __restrict__ yk;
   int i, ext, tw, stages, nc, L0, L1, Lend;
   bool col;
+  double* carry_lo;         // mirrored terms this CTA computes for the previous segment's last p lines (or null)
+  unsigned* flag_lo;       // set once carry_lo is written
+  const double* carry_hi;  // the next segment's carry for this segment's last p lines (or null)
+  unsigned* flag_hi;
+  double cr[P];            // this column's carry, loaded p lines before it is added
   int st, ph;      // band ring: stage of the next chunk and its phase parity
   int xcur, fcur;  // ring slots of line L
   double acc[P + 1];
@@ -582,8 +601,19 @@ struct SweepConsumer {
     // this thread's copies of x(L) and f(L-p) (the group of line L-p) are done
     cp_async_wait<P - 1>();
     if (L < Lend) {
+      // p lines before its end the CTA takes the next segment's carry rows
+      // (published a few lines into that CTA's run, so the wait is short)
+      const bool take = carry_hi && L == L1 - P;
+      if (take && i == 0) {
+        while (ld_acquire(flag_hi) == 0u) __nanosleep(32);
+        *flag_hi = 0u;  // this CTA is its only reader: ready for the next launch
+      }
       // every consumer has stored x(L) and finished line L-1
       asm volatile("bar.sync 1, %0;\n" ::"r"(nc) : "memory");
+      if (take && col) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) cr[q] = __ldcg(carry_hi + q * ext + i);
+      }
       {
         int sx = xcur + P;
         sx -= sx >= NX ? NX : 0;
@@ -610,7 +640,7 @@ struct SweepConsumer {
             }
             // mirrored entries A(r - s, r), s = (m, d0), m = p - q: row r of line L, offset -s
             const int m = P - q;
-            if (L - m >= L0 && L - m < L1) {
+            if (L - m >= 0) {
               const int sa = (PH + 1 + q) % (P + 1);  // slot of line L - m
 #pragma unroll
               for (int d0 = (m == 0 ? 1 : -P); d0 <= P; ++d0)
@@ -630,12 +660,31 @@ struct SweepConsumer {
     }
     constexpr int SW = (PH + 1) % (P + 1);  // slot of line L - p, complete now
     const int Lw = L - P;
-    if (Lw >= L0 && col) {
-      int sf = fcur + 2;  // slot of f(L - p)
-      sf -= sf >= NF ? NF : 0;
-      const double y = fk ? fs[sf * nc + i] - acc[SW] : acc[SW];
-      yk[(size_t)Lw * ext + i] = y;
-      prod = fma(y, xw[SW][P], prod);
+    if (col && Lw >= 0) {
+      if (Lw < L0) {  // mirrored terms of a row of the previous segment
+        carry_lo[(L0 - 1 - Lw) * ext + i] = acc[SW];
+      } else {
+        // rows of the last p lines add the mirrored terms from the next segment's lines
+        double s = acc[SW];
+        if (carry_hi && Lw >= L1 - P) {
+          const int t = L1 - 1 - Lw;
+          double c = 0.0;
+#pragma unroll
+          for (int q = 0; q < P; ++q)
+            if (q == t) c = cr[q];
+          s += c;
+        }
+        int sf = fcur + 2;  // slot of f(L - p)
+        sf -= sf >= NF ? NF : 0;
+        const double y = fk ? fs[sf * nc + i] - s : s;
+        yk[(size_t)Lw * ext + i] = y;
+        prod = fma(y, xw[SW][P], prod);
+      }
+    }
+    if (L == L0 + P - 1 && carry_lo) {  // every carry row is written: publish them
+      __threadfence();
+      asm volatile("bar.sync 1, %0;\n" ::"r"(nc) : "memory");
+      if (i == 0) st_release(flag_lo, 1u);
     }
     acc[SW] = 0.0;  // the accumulator of line L+1
     xcur = xcur + 1 == NX ? 0 : xcur + 1;
@@ -645,10 +694,11 @@ struct SweepConsumer {
 
 template <int P>
 __global__ void __launch_bounds__(kSweepMaxExt + 32, 1) spmv_sweep2d_kernel(SpmvArgs a, SweepCfg g) {
-  PMG_PDL_ENTRY();
+  // no early launch_dependents: a CTA waits for the next segment's CTA, so
+  // dependent grids must not take SMs before every CTA of this one runs
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   constexpr int W = 2 * P + 1;
   constexpr int OB = P * W + P + 1;  // stored offsets: d1 = -p..-1 (all d0), d1 = 0 (d0 <= 0)
-  constexpr int PADL = (P + 1) & ~1;
   using C = SweepConsumer<P>;
   extern __shared__ __align__(128) double smem[];  // [stages][W][tw] band chunks, [NX][tw] x, [NF][nc] f
   __shared__ __align__(8) uint64_t full[kSweepMaxStages], empty[kSweepMaxStages];
@@ -661,10 +711,14 @@ __global__ void __launch_bounds__(kSweepMaxExt + 32, 1) spmv_sweep2d_kernel(Spmv
   const int k = blockIdx.x / g.segs;
   const int L0 = (blockIdx.x - k * g.segs) * g.seglen;
   const int L1 = min(ext, L0 + g.seglen);
-  const int Lend = min(ext, L1 + P);  // streamed lines [L0, Lend)
+  const int Lend = L1;  // streamed lines [L0, L1): each band line crosses HBM once
   const long long S = a.S;
   double* xs = smem + (size_t)stages * W * tw;
   double* fs = xs + C::NX * tw;
+  // segment boundaries of this CTA: b_lo with segment j-1, b_hi with j+1
+  const int jseg = blockIdx.x - k * g.segs;
+  const int b_lo = jseg > 0 ? int(blockIdx.x) : -1;
+  const int b_hi = L1 < ext ? int(blockIdx.x) + 1 : -1;
   const int tid = threadIdx.x;
 
   for (int q = tid; q < C::NX * tw; q += blockDim.x) xs[q] = 0.0;  // x pads
@@ -718,6 +772,10 @@ __global__ void __launch_bounds__(kSweepMaxExt + 32, 1) spmv_sweep2d_kernel(Spmv
   c.L0 = L0;
   c.L1 = L1;
   c.Lend = Lend;
+  c.carry_lo = b_lo >= 0 ? a.sweep_scratch + (size_t)b_lo * P * ext : nullptr;
+  c.flag_lo = b_lo >= 0 ? a.sweep_flags + b_lo : nullptr;
+  c.carry_hi = b_hi >= 0 ? a.sweep_scratch + (size_t)b_hi * P * ext : nullptr;
+  c.flag_hi = b_hi >= 0 ? a.sweep_flags + b_hi : nullptr;
   c.st = 0;
   c.ph = 0;
   c.xcur = 0;
@@ -892,6 +950,16 @@ long long spmv_sweep_band_doubles(int dim, int degree, int ext, long long S, int
   if (!sweep_cfg(dim, degree, ext, S, K, half, sweep, &g, &smem)) return 0;
   const int W = 2 * degree + 1;
   return (long long)K * ext * (degree * W + degree + 1) * g.tw;
+}
+
+void spmv_sweep_scratch(int dim, int degree, int ext, long long S, int K, bool half, int sweep, long long* doubles,
+                        long long* flags) {
+  SweepCfg g;
+  size_t smem;
+  *doubles = *flags = 0;
+  if (!sweep_cfg(dim, degree, ext, S, K, half, sweep, &g, &smem)) return;
+  *flags = (long long)g.segs * K;
+  *doubles = *flags * degree * ext;
 }
 
 void launch_sweep_relayout(cudaStream_t s, int degree, int ext, long long S, int K, long long Sp, const double* src,
