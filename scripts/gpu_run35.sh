@@ -1,2 +1,2 @@
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:fd_pass_dmma -s 0 -c 2 -o gpurun_out/prof_fd4_c2 python scripts/precond_once.py c2 > gpurun_out/ncu_fd4.log 2>&1
-echo "ncu rc=$?"
+timeout 900 python -m pytest tests/test_gpu_parity.py -q --tb=short -x -k "transfers or cycle or pcg" 2>&1 | grep -E "^E  |^FAILED|passed|failed|Error" | head -20
+echo "== tiles"; timeout 600 python scripts/breakdown.py c2 3 2>&1 | grep -E "transfer L[4567]|wall"

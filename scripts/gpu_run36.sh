@@ -1,4 +1,4 @@
-python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('SMOKE OK')" 2>&1 | tail -2
-timeout 2400 python -m pytest tests -m gpu -q --tb=short 2>&1 | grep -E "^E  |^FAILED|passed|failed" | head -10
-timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"; tail -c 3000 gpurun_out/bench_default.json
-timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; cat gpurun_out/bench_ref.json
+for i in 1 2 3 4 5 6; do timeout 600 python -m pytest tests/test_gpu_parity.py -q --tb=no -x -k "c2-p4-L5 and (cycle or transfers)" 2>&1 | grep -E "passed|failed" | head -1; done
+echo "== old"
+cp paper_1804_02539_b200/lib/libpmg_cuda_old.so paper_1804_02539_b200/lib/libpmg_cuda.so
+for i in 1 2 3 4 5 6; do timeout 600 python -m pytest tests/test_gpu_parity.py -q --tb=no -x -k "c2-p4-L5 and (cycle or transfers)" 2>&1 | grep -E "passed|failed" | head -1; done

@@ -1,1 +1,2 @@
-( time timeout 1500 python bench.py --config c5 --steps 2 --warmup 3 --assembly device > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err ) 2>&1 | tail -3; echo "c5 rc=$?"; tail -c 2500 gpurun_out/bench_c5.json; tail -3 gpurun_out/bench_c5.err
+timeout 900 python -m pytest tests/test_gpu_parity.py -q --tb=short -k "transfers or cycle or pcg" 2>&1 | grep -E "^E  |^FAILED|passed|failed|Error" | head -10
+echo "== new"; timeout 600 python scripts/breakdown.py c2 3 2>&1 | grep -E "transfer L[4567]|wall|Error"
