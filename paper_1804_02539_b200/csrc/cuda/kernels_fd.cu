@@ -497,22 +497,34 @@ int fd_rows_per_block() { return kBM * fd_wm(); }
 int fd_pick_ntc(const long long* cols, const long long* weight, int n) {
   // the column-panel width (in n-tiles) with the least padding over the
   // groups; 11 (88 columns) is measured slower than 9 at the c2 finest level
-  // (fewer, larger CTAs per wave) and is only used when forced (PMG_FD_NTC)
+  // (fewer, larger CTAs per wave) and is only used when forced (PMG_FD_NTC).
+  // weight = rows of each group.
   static const int cands[2] = {5, 9};
   int best = 9;
   double best_cost = -1.0;
-  for (int c : cands) {
+  long long ctas[2] = {0, 0};
+  for (int ci = 0; ci < 2; ++ci) {
+    const int c = cands[ci];
     // narrow panels reload A fragments more often per DMMA: measured 0.92x the
     // 72-column rate on c2's finest level, so their padded width costs 1.09x
     const double rate = c == 5 ? 1.09 : 1.0;
     double cost = 0.0;
-    for (int i = 0; i < n; ++i)
+    for (int i = 0; i < n; ++i) {
       cost += rate * double(weight[i]) * double((cols[i] + 8 * c - 1) / (8 * c) * (8 * c));
+      ctas[ci] += (weight[i] + kBM - 1) / kBM * ((cols[i] + 8 * c - 1) / (8 * c));
+    }
     if (best_cost < 0.0 || cost < best_cost || (cost == best_cost && c > best)) {
       best = c;
       best_cost = cost;
     }
   }
+  // a pass that fills fewer than two CTAs per SM is latency-bound: the narrow
+  // panel doubles its CTAs (c2 levels 5-6: 8.4 -> 7.3 and 15.5 -> 14 us per
+  // pass, measured), whatever the padding
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (best == 9 && ctas[1] < 2LL * sms && ctas[0] > ctas[1]) best = 5;
   return best;
 }
 
