@@ -487,7 +487,8 @@ void fd_configure() {
   cudaFuncSetAttribute(smooth_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 #define PMG_FD_ATTR(NT, W) \
   cudaFuncSetAttribute(fd_pass_dmma_kernel<NT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<NT, W>::smem));
-  PMG_FD_ATTR(5, 1) PMG_FD_ATTR(9, 1) PMG_FD_ATTR(11, 1) PMG_FD_ATTR(5, 2) PMG_FD_ATTR(9, 2) PMG_FD_ATTR(11, 2)
+  PMG_FD_ATTR(3, 1) PMG_FD_ATTR(5, 1) PMG_FD_ATTR(9, 1) PMG_FD_ATTR(11, 1) PMG_FD_ATTR(5, 2) PMG_FD_ATTR(9, 2)
+  PMG_FD_ATTR(11, 2)
 #undef PMG_FD_ATTR
 }
 
@@ -499,33 +500,35 @@ int fd_pick_ntc(const long long* cols, const long long* weight, int n) {
   // groups; 11 (88 columns) is measured slower than 9 at the c2 finest level
   // (fewer, larger CTAs per wave) and is only used when forced (PMG_FD_NTC).
   // weight = rows of each group.
-  static const int cands[2] = {5, 9};
-  int best = 9;
-  double best_cost = -1.0;
-  long long ctas[2] = {0, 0};
-  for (int ci = 0; ci < 2; ++ci) {
+  static const int cands[3] = {3, 5, 9};
+  // narrow panels reload A fragments more often per DMMA: measured 0.92x the
+  // 72-column rate on c2's finest level for 40 columns
+  static const double rate[3] = {1.2, 1.09, 1.0};
+  double cost[3] = {0.0, 0.0, 0.0}, pad[3] = {0.0, 0.0, 0.0};
+  long long ctas[3] = {0, 0, 0};
+  double work = 0.0;
+  for (int ci = 0; ci < 3; ++ci) {
     const int c = cands[ci];
-    // narrow panels reload A fragments more often per DMMA: measured 0.92x the
-    // 72-column rate on c2's finest level, so their padded width costs 1.09x
-    const double rate = c == 5 ? 1.09 : 1.0;
-    double cost = 0.0;
     for (int i = 0; i < n; ++i) {
-      cost += rate * double(weight[i]) * double((cols[i] + 8 * c - 1) / (8 * c) * (8 * c));
+      const double w = double((cols[i] + 8 * c - 1) / (8 * c) * (8 * c));
+      cost[ci] += rate[ci] * double(weight[i]) * w;
+      pad[ci] += double(weight[i]) * w;
       ctas[ci] += (weight[i] + kBM - 1) / kBM * ((cols[i] + 8 * c - 1) / (8 * c));
-    }
-    if (best_cost < 0.0 || cost < best_cost || (cost == best_cost && c > best)) {
-      best = c;
-      best_cost = cost;
+      if (ci == 0) work += double(weight[i]) * double(cols[i]);
     }
   }
-  // a pass that fills fewer than two CTAs per SM is latency-bound: the narrow
-  // panel doubles its CTAs (c2 levels 5-6: 8.4 -> 7.3 and 15.5 -> 14 us per
-  // pass, measured), whatever the padding
+  int best = 2;  // 5 and 9 by cost (3 only for parallelism, below)
+  if (cost[1] < cost[2]) best = 1;
+  // a pass that fills fewer than two CTAs per SM is latency-bound: take the
+  // panel with the most CTAs among those padding <= 25% (c2 levels 5-6:
+  // 8.4 -> 7.3 and 15.5 -> 14 us per pass with 40-column panels, measured)
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (best == 9 && ctas[1] < 2LL * sms && ctas[0] > ctas[1]) best = 5;
-  return best;
+  if (ctas[best] < 2LL * sms)
+    for (int ci = 0; ci < 3; ++ci)
+      if (pad[ci] <= 1.25 * work && ctas[ci] > ctas[best]) best = ci;
+  return cands[best];
 }
 
 int fd_wm() {
@@ -547,7 +550,8 @@ void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, in
              pass, naxes, in_mode, out_mode, lat_in, lat_out, alpha, work_in, work_out);                      \
     return;                                                                                                    \
   }
-  PMG_FD_CASE(5, 1) PMG_FD_CASE(9, 1) PMG_FD_CASE(11, 1) PMG_FD_CASE(5, 2) PMG_FD_CASE(9, 2) PMG_FD_CASE(11, 2)
+  PMG_FD_CASE(3, 1) PMG_FD_CASE(5, 1) PMG_FD_CASE(9, 1) PMG_FD_CASE(11, 1) PMG_FD_CASE(5, 2) PMG_FD_CASE(9, 2)
+  PMG_FD_CASE(11, 2)
 #undef PMG_FD_CASE
 }
 
