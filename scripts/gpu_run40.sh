@@ -1,3 +1,2 @@
-python scripts/precond_once.py c4 > /dev/null 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/launches_c4_warm.csv python scripts/precond_once.py c4 > gpurun_out/ncu_c4.log 2>&1
-python scripts/ncu_summary.py gpurun_out/launches_c4_warm.csv > gpurun_out/launches_c4_warm.txt; head -24 gpurun_out/launches_c4_warm.txt
+timeout 1200 python -m pytest tests/test_gpu_parity.py -q --tb=short -k "line_sweep" 2>&1 | grep -E "^E  |^FAILED|passed|failed|Error" | head -10
+echo "== split"; timeout 600 python scripts/breakdown.py c2 3 2>&1 | grep -E "spmv L[67]|wall"
