@@ -654,6 +654,8 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
       }
       const char* fntc = std::getenv("PMG_FD_NTC");
       const int ntc = fntc ? std::atoi(fntc) : fd_pick_ntc(cols.data(), weight.data(), int(groups.size()));
+      if (ntc != 3 && ntc != 5 && ntc != 9 && ntc != 11)
+        throw PmgError(PMG_ERR_CONFIG, "PMG_FD_NTC must be 3, 5, 9 or 11");
       const int BN = 8 * ntc;
       std::vector<int4> it;
       for (const auto& gr : groups) {

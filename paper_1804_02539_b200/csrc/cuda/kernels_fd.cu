@@ -487,8 +487,8 @@ void fd_configure() {
   cudaFuncSetAttribute(smooth_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 #define PMG_FD_ATTR(NT, W) \
   cudaFuncSetAttribute(fd_pass_dmma_kernel<NT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<NT, W>::smem));
-  PMG_FD_ATTR(3, 1) PMG_FD_ATTR(5, 1) PMG_FD_ATTR(9, 1) PMG_FD_ATTR(11, 1) PMG_FD_ATTR(5, 2) PMG_FD_ATTR(9, 2)
-  PMG_FD_ATTR(11, 2)
+  PMG_FD_ATTR(3, 1) PMG_FD_ATTR(5, 1) PMG_FD_ATTR(9, 1) PMG_FD_ATTR(11, 1) PMG_FD_ATTR(3, 2) PMG_FD_ATTR(5, 2)
+  PMG_FD_ATTR(9, 2) PMG_FD_ATTR(11, 2)
 #undef PMG_FD_ATTR
 }
 
@@ -550,9 +550,10 @@ void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, in
              pass, naxes, in_mode, out_mode, lat_in, lat_out, alpha, work_in, work_out);                      \
     return;                                                                                                    \
   }
-  PMG_FD_CASE(3, 1) PMG_FD_CASE(5, 1) PMG_FD_CASE(9, 1) PMG_FD_CASE(11, 1) PMG_FD_CASE(5, 2) PMG_FD_CASE(9, 2)
-  PMG_FD_CASE(11, 2)
+  PMG_FD_CASE(3, 1) PMG_FD_CASE(5, 1) PMG_FD_CASE(9, 1) PMG_FD_CASE(11, 1) PMG_FD_CASE(3, 2) PMG_FD_CASE(5, 2)
+  PMG_FD_CASE(9, 2) PMG_FD_CASE(11, 2)
 #undef PMG_FD_CASE
+  throw std::runtime_error("FD pass: no kernel for this column panel (PMG_FD_NTC must be 3, 5, 9 or 11)");
 }
 
 }  // namespace pmgcu

@@ -1,2 +1,2 @@
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:spmv_tma_half -s 0 -c 1 -o gpurun_out/prof_spmv_c4 python scripts/precond_once.py c4 > gpurun_out/ncu_sc4.log 2>&1
-echo "ncu rc=$?"
+for wm in 1 2; do echo "== wm $wm"; PMG_FD_WM=$wm timeout 600 python scripts/breakdown.py c2 3 2>&1 | grep -E "fd_interior L[567]|wall"; done
+for wm in 1 2; do echo "== c4 wm $wm"; PMG_FD_WM=$wm timeout 600 python scripts/breakdown.py c4 2 2>&1 | grep -E "fd_interior L[45]|wall"; done
