@@ -870,7 +870,10 @@ template <int P>
 bool sweep_cfg_p(int ext, int K, int min_ext, SweepCfg* g, size_t* smem) {
   constexpr int W = 2 * P + 1;
   constexpr int PADL = (P + 1) & ~1;
-  static const int budget = env_int("PMG_SWEEP_SMEM", 200 * 1024);
+  // shared memory per CTA: short lines run several CTAs per SM (their per-line
+  // chain is latency-bound; measured at ext = 132: 33 -> 30 us per launch)
+  static const int budget_env = env_int("PMG_SWEEP_SMEM", 0);
+  const int budget = budget_env > 0 ? budget_env : (ext <= 160 ? 72 * 1024 : 200 * 1024);
   if (ext > kSweepMaxExt || ext < min_ext || ext < 2 * P + 2) return false;
   g->nc = (ext + 31) / 32 * 32;
   g->tw = (PADL + ext + P + 1) & ~1;  // columns PADL - p .. PADL + ext - 1 + p, even (16-byte rows)
