@@ -632,8 +632,6 @@ struct SweepConsumer {
           if (col) {
             const double* T = smem + (size_t)st * W * tw + PADL + i;
             if (L < L1) {  // lower entries of the rows of line L, d1 = q - p (d0 <= 0 at d1 = 0)
-              constexpr int dummy = 0;
-              (void)dummy;
               const int sl = (PH + 1 + q) % (P + 1);  // slot of line L - (p - q)
 #pragma unroll
               for (int w = 0; w < (q < P ? W : P + 1); ++w) acc[PH] = fma(T[w * tw], xw[sl][w], acc[PH]);
