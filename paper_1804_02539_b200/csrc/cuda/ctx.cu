@@ -50,6 +50,7 @@ struct DevLevel {
   double* band = nullptr;
   double* sweep_scratch = nullptr;  // line sweep: segment-boundary rows
   unsigned* sweep_flags = nullptr;
+  unsigned long long* sweep_ticket = nullptr;
   int* l2g = nullptr;
   unsigned char* owner = nullptr;
   int* rep_off = nullptr;
@@ -400,8 +401,12 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
     spmv_sweep_scratch(d, p, L.ext, S, L.K, L.Ob != L.O, c.sweep, &nd, &nf);
     if (nf > 0) {
       L.sweep_scratch = c.alloc<double>(size_t(nd));
-      L.sweep_flags = c.alloc<unsigned>(size_t(nf));
-      ck(cudaMemsetAsync(L.sweep_flags, 0, sizeof(unsigned) * nf, c.stream), "memset");
+      // one flag per segment boundary, then the 64-bit segment ticket counter
+      // at the next even word (cudaMalloc memory is 256-byte aligned)
+      const long long tk = (nf + 1) & ~1LL;
+      L.sweep_flags = c.alloc<unsigned>(size_t(tk + 2));
+      ck(cudaMemsetAsync(L.sweep_flags, 0, sizeof(unsigned) * (tk + 2), c.stream), "memset");
+      L.sweep_ticket = reinterpret_cast<unsigned long long*>(L.sweep_flags + tk);
     }
   }
 
@@ -839,7 +844,7 @@ void op_spmv(pmg_ctx& c, int l, const double* x, const double* f, double* y, dou
     throw PmgError(PMG_ERR_CONFIG, "half-band SpMV needs a 16-byte aligned x (TMA window)");
   TimedScope ts(c, 0, l, bytes);
   SpmvArgs a{c.dim, c.degree, L.ext, L.S, L.K, L.band, x, f, y, dot_partial, L.Ob != L.O, L.Sp, c.sweep,
-             L.sweep_scratch, L.sweep_flags};
+             L.sweep_scratch, L.sweep_flags, L.sweep_ticket};
   launch_spmv(c.stream, a);
   c.launches++;
   c.spmv_launches++;

@@ -120,6 +120,7 @@ struct SpmvArgs {
   int sweep = 128;     // 2D half band: line-sweep kernel on lines of >= sweep rows (0: off)
   double* sweep_scratch = nullptr;  // sweep: per segment boundary, the carry rows (spmv_sweep_scratch)
   unsigned* sweep_flags = nullptr;  // sweep: per segment boundary, carry published (zeroed; reset by the reader)
+  unsigned long long* sweep_ticket = nullptr;  // sweep: segment ticket counter (zeroed, 8-byte aligned)
 };
 void launch_spmv(cudaStream_t s, const SpmvArgs& a);
 int spmv_blocks(long long rows);
@@ -133,6 +134,7 @@ bool spmv_tma_level(int dim, int degree, long long S);
 int spmv_stored_offsets(int dim, int degree, long long S, bool allow_half);
 // number of dot partials one launch writes
 int spmv_partials(int dim, int degree, long long S, int K, bool half, int sweep);
+// scratch of a swept level: carry rows (doubles) and boundary flags (count)
 // 2D line-sweep levels keep the band line-major ([K][ext][Ob][tw], zero
 // padded): its size in doubles (0: the level is not swept), and the
 // conversion from the offset-major band

@@ -702,22 +702,34 @@ __global__ void __launch_bounds__(kSweepMaxExt + 32, 1) spmv_sweep2d_kernel(Spmv
   __shared__ __align__(8) uint64_t full[kSweepMaxStages], empty[kSweepMaxStages];
   __shared__ double red[kSweepMaxExt / 32];
 
+  __shared__ int s_seg;
   const int ext = a.ext;
   const int nc = g.nc;
   const int tw = g.tw;
   const int stages = g.stages;
-  const int k = blockIdx.x / g.segs;
-  const int L0 = (blockIdx.x - k * g.segs) * g.seglen;
+  const int tid = threadIdx.x;
+  // Segments are handed out in the order CTAs start (a ticket counter that
+  // every launch advances by the grid size), last segment of a patch first:
+  // a CTA only ever waits for the carry of the segment above it, which holds
+  // an earlier ticket and so already runs.  No wait depends on how many CTAs
+  // fit on the GPU at once.
+  if (tid == 0) {
+    const unsigned long long t = atomicAdd(a.sweep_ticket, 1ull) % gridDim.x;
+    s_seg = int(t / g.segs) * g.segs + (g.segs - 1 - int(t % g.segs));
+  }
+  __syncthreads();
+  const int seg = s_seg;  // k * segs + j
+  const int k = seg / g.segs;
+  const int jseg = seg - k * g.segs;
+  const int L0 = jseg * g.seglen;
   const int L1 = min(ext, L0 + g.seglen);
   const int Lend = L1;  // streamed lines [L0, L1): each band line crosses HBM once
   const long long S = a.S;
   double* xs = smem + (size_t)stages * W * tw;
   double* fs = xs + C::NX * tw;
-  // segment boundaries of this CTA: b_lo with segment j-1, b_hi with j+1
-  const int jseg = blockIdx.x - k * g.segs;
-  const int b_lo = jseg > 0 ? int(blockIdx.x) : -1;
-  const int b_hi = L1 < ext ? int(blockIdx.x) + 1 : -1;
-  const int tid = threadIdx.x;
+  // segment boundaries: b_lo with segment j-1, b_hi with j+1
+  const int b_lo = jseg > 0 ? seg : -1;
+  const int b_hi = L1 < ext ? seg + 1 : -1;
 
   for (int q = tid; q < C::NX * tw; q += blockDim.x) xs[q] = 0.0;  // x pads
   if (tid == 0) {
@@ -814,7 +826,7 @@ __global__ void __launch_bounds__(kSweepMaxExt + 32, 1) spmv_sweep2d_kernel(Spmv
     if (tid == 0) {
       double sum = 0.0;
       for (int w = 0; w < nc / 32; ++w) sum += red[w];
-      a.dot_partial[blockIdx.x] = sum;
+      a.dot_partial[seg] = sum;  // per segment: the same order of partials every run
     }
   }
 }

@@ -79,3 +79,21 @@ def test_parallel_solve_tracks_serial(hier, R):  # test_parallel.cpp:581-625
     # same partition, same exchange order: a rerun reproduces every bit
     _, rep2, _ = parallel_pcg_solve(h, R, f)
     assert rep2.residual_history == rep.residual_history
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_concurrent_line_sweeps(R, monkeypatch):
+    """R contexts solve at once on one GPU with the 2D line sweep on every
+    level (PMG_SWEEP_MIN_EXT=1): each rank's sweep grid is sized to fill the
+    GPU alone, so the grids compete for SMs.  A sweep CTA waits for the carry
+    of the segment above it; segments are handed out in CTA start order, so the
+    wait never depends on co-residency.  The solve must finish and match the
+    serial iteration count and solution."""
+    monkeypatch.setenv("PMG_SWEEP_MIN_EXT", "1")
+    h = Hierarchy("c2", 4, 5, n0=2)
+    o = oracle.Oracle(h)
+    f = h.rhs()
+    u_ref, hist_ref, _, _ = o.pcg_solve(f)
+    u, rep, _ = parallel_pcg_solve(h, R, f)
+    assert rep.iterations == len(hist_ref) - 1
+    assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
