@@ -713,10 +713,21 @@ __global__ void __launch_bounds__(kSweepMaxExt + 32, 1) spmv_sweep2d_kernel(Spmv
   // a CTA only ever waits for the carry of the segment above it, which holds
   // an earlier ticket and so already runs.  No wait depends on how many CTAs
   // fit on the GPU at once.
+  // (the ticket's round trip overlaps the pad zeroing and barrier setup)
+  unsigned long long ticket = 0;
+  if (tid == 0) ticket = atomicAdd(a.sweep_ticket, 1ull);
+  double* xs = smem + (size_t)stages * W * tw;
+  for (int q = tid; q < C::NX * tw; q += blockDim.x) xs[q] = 0.0;  // x pads
   if (tid == 0) {
-    const unsigned long long t = atomicAdd(a.sweep_ticket, 1ull) % gridDim.x;
+    for (int st = 0; st < stages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], nc / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    const unsigned long long t = ticket % gridDim.x;
     s_seg = int(t / g.segs) * g.segs + (g.segs - 1 - int(t % g.segs));
   }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   __syncthreads();
   const int seg = s_seg;  // k * segs + j
   const int k = seg / g.segs;
@@ -725,22 +736,10 @@ __global__ void __launch_bounds__(kSweepMaxExt + 32, 1) spmv_sweep2d_kernel(Spmv
   const int L1 = min(ext, L0 + g.seglen);
   const int Lend = L1;  // streamed lines [L0, L1): each band line crosses HBM once
   const long long S = a.S;
-  double* xs = smem + (size_t)stages * W * tw;
   double* fs = xs + C::NX * tw;
   // segment boundaries: b_lo with segment j-1, b_hi with j+1
   const int b_lo = jseg > 0 ? seg : -1;
   const int b_hi = L1 < ext ? seg + 1 : -1;
-
-  for (int q = tid; q < C::NX * tw; q += blockDim.x) xs[q] = 0.0;  // x pads
-  if (tid == 0) {
-    for (int st = 0; st < stages; ++st) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], nc / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  __syncthreads();
 
   if (tid >= nc) {  // producer thread: one bulk copy per chunk
     if (tid == nc) {

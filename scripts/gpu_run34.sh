@@ -8,5 +8,5 @@ timeout 1200 python bench.py --config c5 --steps 2 --warmup 3 --no-cpu-baseline 
 python scripts/solve_once.py c2 2 > gpurun_out/solve_once.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/launches_c2_warm.csv python scripts/solve_once.py c2 2 > gpurun_out/ncu_c2.log 2>&1
 python scripts/ncu_summary.py gpurun_out/launches_c2_warm.csv > gpurun_out/launches_c2_warm.txt; head -8 gpurun_out/launches_c2_warm.txt
-ncu --set full --clock-control none --import-source on -k regex:sweep2d -c 1 -o gpurun_out/prof_sweep5_c2 python scripts/solve_once.py c2 1 > gpurun_out/ncu_sweep.log 2>&1; echo "rc=$?"
-ncu -i gpurun_out/prof_sweep5_c2.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 2>&1 | tail -1
+ncu --set full --clock-control none --import-source on -k regex:sweep2d -c 1 -o gpurun_out/prof_sweep6_c2 python scripts/solve_once.py c2 1 > gpurun_out/ncu_sweep.log 2>&1; echo "rc=$?"
+ncu -i gpurun_out/prof_sweep6_c2.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 2>&1 | tail -1
