@@ -34,7 +34,9 @@ WORKLOADS = {
     "c1": "2D Poisson, 2x2 affine patches, p=2, 64^2 elements/patch (BASELINE config 1)",
     "c2": "2D Poisson, 4x4 sinusoidally perturbed patches, p=4, 256^2 elements/patch (BASELINE config 2)",
     "c3p2": "2D 4x4 patches, p=2, 128^2 elements/patch (BASELINE config 3)",
+    "c3p3": "2D 4x4 patches, p=3, 128^2 elements/patch (BASELINE config 3)",
     "c3p4": "2D 4x4 patches, p=4, 128^2 elements/patch (BASELINE config 3)",
+    "c3p6": "2D 4x4 patches, p=6, 128^2 elements/patch (BASELINE config 3)",
     "c3p8": "2D 4x4 patches, p=8, 128^2 elements/patch (BASELINE config 3)",
     "c4": "3D Poisson, 2x2x2 jittered trilinear patches, p=3, 64^3 elements/patch (BASELINE config 4)",
     "c5": "3D Poisson, 4x4x2 jittered trilinear patches, p=3, 64^3 elements/patch (BASELINE config 5)",

@@ -42,6 +42,7 @@ CASES = [
     # symmetric half-band SpMV and the DMMA fast-diagonalization passes
     ("c1", 2, 5, 2, "default"),
     ("c2", 4, 5, 2, "default"),
+    ("c3", 3, 5, 2, "default"),
     ("c3", 6, 5, 2, "default"),
     ("c3", 8, 5, 2, "default"),
     ("c4", 3, 3, 2, "default"),
