@@ -32,9 +32,16 @@ namespace {
 
 constexpr int kFdThreads = 128;
 constexpr int kBM = 32;          // rows per CTA (4 warps x 8)
-constexpr int kBK = 16;          // k per shared-memory stage
+#ifndef PMG_FD_BK
+#define PMG_FD_BK 16
+#endif
+#ifndef PMG_FD_STAGES
+#define PMG_FD_STAGES 3
+#endif
+constexpr int kBK = PMG_FD_BK;   // k per shared-memory stage
 constexpr int kXS = kBK + 4;     // X row stride (doubles): conflict-free A fragments
-constexpr int kStagesFd = 3;
+constexpr int kStagesFd = PMG_FD_STAGES;
+constexpr int kXRowStep = kFdThreads / kBK;  // X rows covered by one copy round
 
 // column panel of NTC n-tiles (8 columns each); B row stride = 4 mod 16
 // doubles so the 4 x 8 B-fragment reads of a half-warp hit distinct banks
@@ -154,7 +161,7 @@ __global__ void __launch_bounds__(kFdThreads, WM == 1 ? 4 : 2) fd_pass_dmma_kern
   bool xrow_ok[T::XPer];
 #pragma unroll
   for (int j = 0; j < T::XPer; ++j) {
-    const long long r = r0 + tid / kBK + 8 * j;
+    const long long r = r0 + tid / kBK + kXRowStep * j;
     xrow_ok[j] = r < rows;
     const long long rg = xrow_ok[j] ? r : 0;
     const FdPiece& P = pieces[it.x + int(rg / R)];
@@ -181,7 +188,7 @@ __global__ void __launch_bounds__(kFdThreads, WM == 1 ? 4 : 2) fd_pass_dmma_kern
 #pragma unroll
     for (int j = 0; j < T::XPer; ++j) {
       const bool ok = xrow_ok[j] && k0 + xk < K;
-      cp_async8(xs + (tid / kBK + 8 * j) * kXS + xk, ok ? xsrc[j] + k0 : B, ok);
+      cp_async8(xs + (tid / kBK + kXRowStep * j) * kXS + xk, ok ? xsrc[j] + k0 : B, ok);
     }
 #pragma unroll
     for (int j = 0; j < T::BPer; ++j) {
