@@ -1,0 +1,83 @@
+"""Size-independent properties of the CUDA path at BASELINE.json's full sizes
+(c2: 1,071,225 dofs; c4: 2,317,259 dofs), where the oracle is too slow to be
+the per-case checker:
+
+  operator    symmetry x.(A y) = y.(A x) and linearity A(x + 2y) = Ax + 2Ay
+              (the Galerkin stiffness is SPD, test_assembly.cpp:174-203)
+  V-cycle     the V(1,1) preconditioner with the symmetric smoother and no
+              coarse damping is symmetric and positive (the PCG contract of
+              multigrid.hpp:155-189)
+  PCG         the recursive residual meets tol 1e-8 (multigrid.hpp:180) and
+              the true residual ||f - A u|| / ||f|| agrees with it
+  rerun       two solves on the same context are bitwise identical
+
+c4 is assembled on the device (the host assembly takes ~30 s)."""
+import numpy as np
+import pytest
+
+from paper_1804_02539_b200.hierarchy import CONFIGS, Hierarchy
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", params=[("c2", "host"), ("c4", "device")], ids=["c2", "c4"])
+def full(request):
+    from paper_1804_02539_b200.backend import GpuBackend
+
+    name, assembly = request.param
+    dom, p, n0, lv = CONFIGS[name]
+    h = Hierarchy(dom, p, lv, n0=n0, assembly=assembly)
+    b = GpuBackend(h)
+    yield h, b
+    b.close()
+
+
+def rng_vec(n, seed):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+def test_operator_symmetric_and_linear(full):
+    h, b = full
+    L = h.finest_level
+    n = h.num_dofs(L)
+    x, y = rng_vec(n, 1), rng_vec(n, 2)
+    ax = b.apply_op(L, b.to_accumulated(L, x))
+    ay = b.apply_op(L, b.to_accumulated(L, y))
+    xay = b.dot(L, ay, b.to_accumulated(L, x))
+    yax = b.dot(L, ax, b.to_accumulated(L, y))
+    scale = np.sqrt(b.dot(L, ax, b.to_accumulated(L, x)) * b.dot(L, ay, b.to_accumulated(L, y)))
+    assert abs(xay - yax) <= 1e-12 * scale
+    axy = b.gather_global(L, b.apply_op(L, b.to_accumulated(L, x + 2.0 * y)))
+    lin = b.gather_global(L, ax) + 2.0 * b.gather_global(L, ay)
+    assert np.abs(axy - lin).max() <= 1e-13 * np.abs(lin).max() * 8
+
+
+def test_preconditioner_symmetric_positive(full):
+    h, b = full
+    L = h.finest_level
+    n = h.num_dofs(L)
+    x, y = rng_vec(n, 3), rng_vec(n, 4)
+    cx = b.precondition(b.to_distributed_owner(L, x))
+    cy = b.precondition(b.to_distributed_owner(L, y))
+    ycx = b.dot(L, b.to_distributed_owner(L, y), cx)
+    xcy = b.dot(L, b.to_distributed_owner(L, x), cy)
+    xcx = b.dot(L, b.to_distributed_owner(L, x), cx)
+    ycy = b.dot(L, b.to_distributed_owner(L, y), cy)
+    assert xcx > 0.0 and ycy > 0.0
+    assert abs(ycx - xcy) <= 1e-10 * np.sqrt(xcx * ycy)
+
+
+def test_pcg_converges_and_reruns_bitwise(full):
+    h, b = full
+    L = h.finest_level
+    f = h.rhs()
+    u, rep = b.pcg_solve(f)
+    hist = np.array(rep.residual_history)
+    assert rep.iterations == len(hist) - 1 and 0 < rep.iterations < 60
+    assert hist[-1] <= 1e-8 * hist[0]
+    r = b.gather_global(L, b.residual(L, b.to_distributed_owner(L, f), b.to_accumulated(L, u)))
+    assert np.linalg.norm(r) <= 2e-8 * np.linalg.norm(f)
+    u2, rep2 = b.pcg_solve(f)
+    assert rep2.iterations == rep.iterations
+    assert np.array_equal(u2, u)
+    assert np.array_equal(np.array(rep2.residual_history), hist)
