@@ -1,6 +1,6 @@
 """Size-independent properties of the CUDA path at BASELINE.json's full sizes
-(c2: 1,071,225 dofs; c4: 2,317,259 dofs), where the oracle is too slow to be
-the per-case checker:
+(c2: 1,071,225 dofs; c3 at p = 8; c4: 2,317,259 dofs; c5: 9,269,435 dofs),
+where the oracle is too slow to be the per-case checker:
 
   operator    symmetry x.(A y) = y.(A x) and linearity A(x + 2y) = Ax + 2Ay
               (the Galerkin stiffness is SPD, test_assembly.cpp:174-203)
@@ -11,7 +11,7 @@ the per-case checker:
               the true residual ||f - A u|| / ||f|| agrees with it
   rerun       two solves on the same context are bitwise identical
 
-c4 is assembled on the device (the host assembly takes ~30 s)."""
+c4 and c5 are assembled on the device (the host assembly of c4 takes ~30 s)."""
 import numpy as np
 import pytest
 
@@ -20,7 +20,8 @@ from paper_1804_02539_b200.hierarchy import CONFIGS, Hierarchy
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=[("c2", "host"), ("c4", "device")], ids=["c2", "c4"])
+@pytest.fixture(scope="module", params=[("c2", "host"), ("c3p8", "host"), ("c4", "device"), ("c5", "device")],
+                ids=["c2", "c3p8", "c4", "c5"])
 def full(request):
     from paper_1804_02539_b200.backend import GpuBackend
 
