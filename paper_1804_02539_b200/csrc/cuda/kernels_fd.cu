@@ -35,6 +35,9 @@ constexpr int kBM = 32;          // rows per CTA (4 warps x 8)
 #ifndef PMG_FD_BK
 #define PMG_FD_BK 16
 #endif
+#ifndef PMG_FD_MINB
+#define PMG_FD_MINB 4
+#endif
 #ifndef PMG_FD_STAGES
 #define PMG_FD_STAGES 3
 #endif
@@ -127,7 +130,7 @@ __device__ __forceinline__ void fd_epilogue(const FdPiece& P, long long rl, cons
 // dimension has no per-piece padding).  item = (first piece of the group,
 // first row of the panel within the group, first column, rows of the group).
 template <int NTC, int WM>
-__global__ void __launch_bounds__(kFdThreads, WM == 1 ? 4 : 2) fd_pass_dmma_kernel(const FdPiece* __restrict__ pieces,
+__global__ void __launch_bounds__(kFdThreads, WM == 1 ? PMG_FD_MINB : 2) fd_pass_dmma_kernel(const FdPiece* __restrict__ pieces,
                                                                   const int4* __restrict__ items, int pass,
                                                                   int naxes, int in_mode, int out_mode,
                                                                   const double* __restrict__ lat_in,
