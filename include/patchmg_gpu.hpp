@@ -6,9 +6,18 @@
 // multigrid.hpp:120-189), with the same method names, argument meaning and
 // error behaviour as SerialBackend (multigrid.hpp:80-114) and ParallelBackend
 // (parallel.hpp:267-341): AccVec / DistVec are distinct RAII device-vector
-// handles, status codes are rethrown as the reference's exception classes
-// (errors.hpp:9-56).  The templates below are written against the concept
-// only, exactly as the reference's are, so either can drive this backend.
+// handles, status codes are rethrown as exception classes.
+//
+// BasicGpuBackend<Params, Errors> is parametrised on the parameter struct that
+// params() returns and on the exception policy.  GpuBackend uses this
+// header's own CycleParams and exception classes (standalone builds);
+// include/patchmg_gpu_reference.hpp binds patchmg::CycleParams and the
+// reference's patchmg:: exceptions (errors.hpp:9-56), so the reference's own
+// templates -- patchmg::pcg_generic / mg_precondition / mg_cycle_generic from
+// multigrid.hpp:120-189, compiled unchanged -- drive it
+// (oracle/ref_templates/pcg_ref_templates.cpp, tests/test_gpu_cpp_dropin.py).
+// The restated templates at the end of this header are for builds without the
+// reference's headers.
 #pragma once
 
 #include <cmath>
@@ -30,6 +39,7 @@ struct DivergenceError : Error { using Error::Error; };
 struct TransportError : Error { using Error::Error; };
 struct CudaError : Error { using Error::Error; };
 
+// status code -> exception (this header's classes)
 inline void check(int rc, const char* msg) {
   switch (rc) {
     case PMG_OK: return;
@@ -44,23 +54,27 @@ inline void check(int rc, const char* msg) {
   }
 }
 
+struct NativeErrors {
+  static void raise(int rc, const char* msg) { check(rc, msg); }
+};
+
 struct CycleParams {  // multigrid.hpp:21-27
   int nu = 1, mu = 1;
   double tau = 0.25, sigma_scale = 0.2;
   bool damp_coarse = false;
 };
 
-template <int Form>
+template <int Form, class Errors = NativeErrors>
 class DeviceVector {  // AccumulatedVector / DistributedVector, parallel.hpp:169-260
  public:
   DeviceVector() = default;
   DeviceVector(pmg_ctx* ctx, int level) : ctx_(ctx), level_(level) {
     pmg_vec* v = nullptr;
-    check(pmg_vec_create(ctx, level, &v), pmg_last_error(ctx));
+    Errors::raise(pmg_vec_create(ctx, level, &v), pmg_last_error(ctx));
     v_ = v;
   }
   DeviceVector(const DeviceVector& o) : DeviceVector(o.ctx_, o.level_) {
-    check(pmg_vec_copy(ctx_, o.v_, v_), pmg_last_error(ctx_));
+    Errors::raise(pmg_vec_copy(ctx_, o.v_, v_), pmg_last_error(ctx_));
   }
   DeviceVector& operator=(const DeviceVector& o) {
     if (this != &o) {
@@ -68,7 +82,7 @@ class DeviceVector {  // AccumulatedVector / DistributedVector, parallel.hpp:169
         DeviceVector tmp(o.ctx_, o.level_);
         swap(tmp);
       }
-      check(pmg_vec_copy(ctx_, o.v_, v_), pmg_last_error(ctx_));
+      Errors::raise(pmg_vec_copy(ctx_, o.v_, v_), pmg_last_error(ctx_));
     }
     return *this;
   }
@@ -95,25 +109,26 @@ class DeviceVector {  // AccumulatedVector / DistributedVector, parallel.hpp:169
   int level_ = -1;
 };
 
-class GpuBackend {
+template <class Params = CycleParams, class Errors = NativeErrors>
+class BasicGpuBackend {
  public:
-  using AccVec = DeviceVector<PMG_ACCUMULATED>;
-  using DistVec = DeviceVector<PMG_DISTRIBUTED>;
+  using AccVec = DeviceVector<PMG_ACCUMULATED, Errors>;
+  using DistVec = DeviceVector<PMG_DISTRIBUTED, Errors>;
 
-  GpuBackend(const pmg_hierarchy_desc& h, int device = 0, const pmg_comm_desc* comm = nullptr) {
+  BasicGpuBackend(const pmg_hierarchy_desc& h, int device = 0, const pmg_comm_desc* comm = nullptr) {
     prm_.nu = h.params.nu;
     prm_.mu = h.params.mu;
     prm_.tau = h.params.tau;
     prm_.sigma_scale = h.params.sigma_scale;
     prm_.damp_coarse = h.params.damp_coarse != 0;
     finest_ = h.num_levels - 1;
-    check(pmg_ctx_create(&h, device, comm, &ctx_), pmg_last_error(nullptr));
+    Errors::raise(pmg_ctx_create(&h, device, comm, &ctx_), pmg_last_error(nullptr));
   }
-  GpuBackend(const GpuBackend&) = delete;
-  GpuBackend& operator=(const GpuBackend&) = delete;
-  ~GpuBackend() { pmg_ctx_destroy(ctx_); }
+  BasicGpuBackend(const BasicGpuBackend&) = delete;
+  BasicGpuBackend& operator=(const BasicGpuBackend&) = delete;
+  ~BasicGpuBackend() { pmg_ctx_destroy(ctx_); }
 
-  const CycleParams& params() const { return prm_; }
+  const Params& params() const { return prm_; }
   int finest_level() const { return finest_; }
   pmg_ctx* ctx() const { return ctx_; }
 
@@ -172,20 +187,27 @@ class GpuBackend {
     return v;
   }
   template <int F>
-  std::vector<double> gather_global(int level, const DeviceVector<F>& v, int64_t n) const {
+  std::vector<double> gather_global(int level, const DeviceVector<F, Errors>& v, int64_t n) const {
     std::vector<double> out(static_cast<size_t>(n));
     ok(pmg_vec_download(ctx_, v.get(), F, out.data(), n));
     return out;
   }
 
  private:
-  void ok(int rc) const { check(rc, pmg_last_error(ctx_)); }
+  void ok(int rc) const { Errors::raise(rc, pmg_last_error(ctx_)); }
   pmg_ctx* ctx_ = nullptr;
-  CycleParams prm_;
+  Params prm_;
   int finest_ = 0;
 };
 
-// ---- the reference's templates, restated against the concept only
+using GpuBackend = BasicGpuBackend<>;
+
+// ---- the reference's templates, restated against the concept only, for
+// builds without the reference's headers.  A nested namespace keeps them out
+// of argument-dependent lookup, so a TU that also includes the reference's
+// multigrid.hpp calls patchmg::pcg_generic & co. unambiguously.
+namespace generic {
+
 template <class B>
 void mg_cycle_generic(const B& b, int level, typename B::AccVec& u, const typename B::DistVec& f) {
   const auto& prm = b.params();
@@ -247,4 +269,5 @@ typename B::AccVec pcg_generic(const B& b, const typename B::DistVec& f, double 
   throw DivergenceError("pcg: no convergence within the iteration limit");
 }
 
+}  // namespace generic
 }  // namespace patchmg_gpu

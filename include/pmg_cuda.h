@@ -71,8 +71,18 @@ void pmg_ctx_destroy(pmg_ctx* ctx);
 const char* pmg_last_error(pmg_ctx* ctx);
 /* what: 0 finest level, 1 lattice slots of level `level`, 2 device bytes held,
  *       3 num_dofs of level `level`, 4 local patches, 5 microseconds spent in
- *       device stiffness assembly (PMG_BAND_ASSEMBLE levels).  level = what >> 8. */
+ *       device stiffness assembly (PMG_BAND_ASSEMBLE levels), 6 collectives
+ *       issued through the rank transport (a captured one counts once).
+ *       level = what >> 8. */
 int pmg_ctx_info(pmg_ctx* ctx, int what, int64_t* out);
+/* The operator of `level` as held on the device, expanded to the reference's
+ * index-free full band double[K_local][(2p+1)^d][(n+p)^d] (the host layout of
+ * pmg_level_desc.band, PMG_BAND_TENSOR; the stored values behind
+ * PatchOperator::apply_add, assembly.hpp:16-25).  The upper half of a
+ * symmetric half band is the mirrored lower entry.  This is how a hierarchy
+ * assembled on the device (PMG_BAND_ASSEMBLE) hands its stiffness to a host
+ * consumer -- the CPU checker and baseline.  n = K_local (2p+1)^d (n+p)^d. */
+int pmg_band_download(pmg_ctx* ctx, int level, double* host, int64_t n);
 /* Launch everything on this cudaStream_t from now on (NULL: the ctx stream). */
 int pmg_set_stream(pmg_ctx* ctx, void* stream);
 int pmg_synchronize(pmg_ctx* ctx);
@@ -134,12 +144,20 @@ int pmg_pcg_solve(pmg_ctx* ctx, const double* f_host, int64_t n, double tol, int
 int pmg_kernel_stats(pmg_ctx* ctx, int which, int64_t* count, double* reserved);
 
 /* Live kernel timing with CUDA events on the launch stream.  While enabled,
- * every launch of the timed classes is bracketed by two events.
- * kernel_class: 0 = band SpMV, 1 = fast-diagonalization pass.
+ * every launch of the timed classes is bracketed by two events, kernels are
+ * launched directly (no graphs) and a PCG solve stops exactly as
+ * pcg_generic does, so an instrumented solve runs the same kernels as the
+ * graph-replayed one.
+ * kernel_class: 0 = band SpMV, 1 = fast-diagonalization pass, 2 = transfer
+ * (restriction / prolongation), 3 = interface pieces of a smooth (Sigma,
+ * face / edge / vertex solves; side stream), 4 = dot / accumulate,
+ * 5 = coarse solve.
  * pmg_profile_read synchronizes and returns, for launches on `level` since the
  * last read: the launch count, the summed device milliseconds and the summed
- * algorithmic bytes (SpMV: 8 B per stored reference entry + 8 B per lattice
- * row for x, y and f when read) or flops (FD: 2 per multiply-add). */
+ * algorithmic work: SpMV bytes = 8 B per stored band entry (the symmetric half
+ * band: (S + D) / 2 entries, S = reference CSR entries, D = lattice rows;
+ * SURVEY 8(d)) + 8 B per lattice row for x, y (and f when read); FD flops =
+ * 2 per multiply-add; 0 for the other classes. */
 int pmg_profile(pmg_ctx* ctx, int enable);
 int pmg_profile_read(pmg_ctx* ctx, int kernel_class, int level, int64_t* launches, double* ms, double* work);
 

@@ -42,6 +42,7 @@ def _load():
             ("oracle_restrict", [_vp, C.c_int, _dp, _dp]),
             ("oracle_add_prolonged", [_vp, C.c_int, _dp, C.c_double, _dp]),
             ("oracle_coarse_solve", [_vp, _dp, _dp]),
+            ("oracle_set_coarse_mode", [_vp, C.c_int]),
             ("oracle_mg_cycle", [_vp, C.c_int, _dp, _dp]),
             ("oracle_precondition", [_vp, _dp, _dp]),
             ("oracle_pcg_solve", [_vp, _dp, C.c_double, C.c_int, C.c_int, _dp, _dp, C.POINTER(C.c_int), _dp]),
@@ -119,6 +120,10 @@ class Oracle:
         u = self._vec(u, self.n(level)).copy()
         self._check(_load().oracle_add_prolonged(self._ctx, level, _p(self._vec(coarse, self.n(level - 1))), c, _p(u)))
         return u
+
+    def set_coarse_mode(self, mode: int):
+        """0: dense LLT substitution (default); 1: explicit inverse GEMV."""
+        self._check(_load().oracle_set_coarse_mode(self._ctx, mode))
 
     def coarse_solve(self, r):
         out = np.empty(self.n(0))

@@ -51,6 +51,11 @@ struct Hier {
   std::vector<Level> lv;
   int n0 = 0;
   const double* L0 = nullptr;
+  // coarse_mode 1: the explicit inverse L^-T L^-1 applied as a GEMV, a
+  // second exact coarse solver with different rounding (measures the
+  // conditioning limit kappa(A_0) eps of any coarse-solve pairing)
+  int coarse_mode = 0;
+  std::vector<double> Ainv;
   int finest() const { return int(lv.size()) - 1; }
 };
 
@@ -348,6 +353,15 @@ Vec restrict_full(const Hier& H, int level, const Vec& fine) {
 Vec coarse_solve(const Hier& H, const Vec& rhs) {
   const int n = H.n0;
   const double* L = H.L0;
+  if (H.coarse_mode == 1) {
+    Vec y(std::size_t(n), 0.0);
+    for (int i = 0; i < n; ++i) {
+      double s = 0.0;
+      for (int k = 0; k < n; ++k) s += H.Ainv[std::size_t(i) * n + k] * rhs[k];
+      y[i] = s;
+    }
+    return y;
+  }
   Vec x = rhs;
   for (int i = 0; i < n; ++i) {
     double s = x[i];
@@ -927,6 +941,35 @@ int oracle_add_prolonged(oracle_ctx* ctx, int level, const double* coarse, doubl
     Vec uu = to_vec(u, ctx->h.lv[level].N);
     b.add_prolonged(level, to_vec(coarse, ctx->h.lv[level - 1].N), c, uu);
     from_vec(uu, u);
+  });
+}
+
+int oracle_set_coarse_mode(oracle_ctx* ctx, int mode) {
+  return guarded([&] {
+    if (mode != 0 && mode != 1) throw ConfigError("coarse mode must be 0 (LLT) or 1 (explicit inverse)");
+    Hier& H = ctx->h;
+    if (mode == 1 && H.Ainv.empty()) {
+      // A0^-1 = L^-T L^-1 from the column-major lower factor
+      const int n = H.n0;
+      const double* L = H.L0;
+      std::vector<double> Li(std::size_t(n) * n, 0.0);  // column-major lower inverse
+      for (int j = 0; j < n; ++j) {
+        Li[std::size_t(j) * n + j] = 1.0 / L[std::size_t(j) * n + j];
+        for (int i = j + 1; i < n; ++i) {
+          double s = 0.0;
+          for (int k = j; k < i; ++k) s += L[std::size_t(k) * n + i] * Li[std::size_t(j) * n + k];
+          Li[std::size_t(j) * n + i] = -s / L[std::size_t(i) * n + i];
+        }
+      }
+      H.Ainv.assign(std::size_t(n) * n, 0.0);
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j <= i; ++j) {
+          double s = 0.0;
+          for (int k = i; k < n; ++k) s += Li[std::size_t(i) * n + k] * Li[std::size_t(j) * n + k];
+          H.Ainv[std::size_t(i) * n + j] = H.Ainv[std::size_t(j) * n + i] = s;
+        }
+    }
+    H.coarse_mode = mode;
   });
 }
 

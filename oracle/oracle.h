@@ -52,6 +52,13 @@ int oracle_coarse_solve(oracle_ctx* ctx, const double* r, double* out);
 int oracle_mg_cycle(oracle_ctx* ctx, int level, double* u, const double* f);
 int oracle_precondition(oracle_ctx* ctx, const double* r, double* z);
 
+/* Coarse solver of this context: 0 the dense LLT substitution (default,
+ * Hierarchy::coarse_solve), 1 the explicit inverse L^-T L^-1 as a GEMV -- a
+ * second exact solver with different rounding, used by the tests to measure
+ * the conditioning limit kappa(A_0) eps that any two exact coarse solvers
+ * differ by (the CUDA path applies the explicit inverse). */
+int oracle_set_coarse_mode(oracle_ctx* ctx, int mode);
+
 /* pcg_generic with the V-cycle preconditioner (multigrid.cpp:72-89).
  * history has room for max_iter+1 entries.  With allow_cap != 0 the
  * iteration cap returns PMG_OK instead of PMG_ERR_DIVERGENCE (bounded CPU

@@ -114,6 +114,16 @@ class GpuBackend:
         self._check(self._lib.pmg_ctx_info(self._ctx, 5, C.byref(n)))
         return n.value / 1e6
 
+    def download_band(self, level: int) -> np.ndarray:
+        """The level's operator as held on the device, as the reference's
+        index-free full band [K_local][(2p+1)^d][(n+p)^d] (pmg_band_download)."""
+        h = self.h
+        k = (self.h.num_patches if self.comm is None else self.comm.patch_end - self.comm.patch_begin)
+        n = k * (2 * h.degree + 1) ** h.dim * h.lattice_size(level)
+        out = np.empty(n)
+        self._check(self._lib.pmg_band_download(self._ctx, level, out.ctypes.data_as(N._dp), n))
+        return out.reshape(k, (2 * h.degree + 1) ** h.dim, h.lattice_size(level))
+
     def lattice_size(self, level: int) -> int:
         n = C.c_int64()
         self._check(self._lib.pmg_ctx_info(self._ctx, (level << 8) | 1, C.byref(n)))
@@ -221,9 +231,12 @@ class GpuBackend:
         _need(f, DistVec, level)
         self._check(self._lib.pmg_mg_cycle(self._ctx, level, u._h, f._h))
 
-    def precondition(self, r: DistVec) -> AccVec:
+    def precondition(self, r: DistVec, out: AccVec | None = None) -> AccVec:
+        """mg_precondition (multigrid.hpp:144-149); `out` reuses a vector (the
+        library replays one cached graph per (r, z) pair)."""
         _need(r, DistVec, self.finest_level())
-        z = AccVec(self, r.level)
+        z = AccVec(self, r.level) if out is None else out
+        _need(z, AccVec, r.level)
         self._check(self._lib.pmg_precondition(self._ctx, r._h, z._h))
         return z
 

@@ -86,11 +86,33 @@ def build_example(force: bool = False) -> Path:
     return out
 
 
+REF_INCLUDE = Path("/root/reference/proj/include")
+REF_TEMPLATES = ROOT / "oracle" / "_ref" / "pcg_ref_templates"
+
+
+def build_ref_templates(force: bool = False):
+    """oracle/_ref/pcg_ref_templates: the reference's own multigrid.hpp
+    templates over the GPU backend (oracle/ref_templates/build.sh).  Built only
+    where the reference tree exists (this container); the binary travels to the
+    GPU box.  Returns the path, or None when the reference is absent."""
+    if not (REF_INCLUDE / "patchmg" / "multigrid.hpp").exists():
+        return REF_TEMPLATES if REF_TEMPLATES.exists() else None
+    host, cuda = build_host(force), build_cuda(force)
+    src = ROOT / "oracle" / "ref_templates"
+    deps = list(src.rglob("*")) + [host, cuda, ROOT / "include" / "patchmg_gpu.hpp",
+                                   ROOT / "include" / "patchmg_gpu_reference.hpp"]
+    if force or not REF_TEMPLATES.exists() or any(
+            d.is_file() and d.stat().st_mtime > REF_TEMPLATES.stat().st_mtime for d in deps):
+        _run(["bash", src / "build.sh"])
+    return REF_TEMPLATES
+
+
 def build_all(force: bool = False) -> None:
     build_host(force)
     build_oracle(force)
     build_cuda(force)
     build_example(force)
+    build_ref_templates(force)
 
 
 if __name__ == "__main__":

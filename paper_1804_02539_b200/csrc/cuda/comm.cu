@@ -40,6 +40,7 @@ class HubTransport final : public Transport {
   uint64_t bytes_sent() const override { return bytes_; }
 
   void exchange(cudaStream_t s, const std::vector<Peer>& peers) override {
+    calls++;
     collective(
         s, [&](Hub::Slot& slot) { slot.posted[rank_] = peers; },
         [&](Hub::Slot& slot) {
@@ -55,6 +56,7 @@ class HubTransport final : public Transport {
         });
   }
   void allgather(cudaStream_t s, const double* in, double* out, size_t n) override {
+    calls++;
     collective(
         s, [&](Hub::Slot& slot) { slot.ptr[rank_] = in; },
         [&](Hub::Slot& slot) {
@@ -64,6 +66,7 @@ class HubTransport final : public Transport {
         });
   }
   void gather(cudaStream_t s, const double* in, double* out, size_t n, int root) override {
+    calls++;
     collective(
         s, [&](Hub::Slot& slot) { slot.ptr[rank_] = in; },
         [&](Hub::Slot& slot) {
@@ -76,6 +79,7 @@ class HubTransport final : public Transport {
         });
   }
   void broadcast(cudaStream_t s, double* buf, size_t n, int root) override {
+    calls++;
     collective(
         s, [&](Hub::Slot& slot) { slot.ptr[rank_] = buf; },
         [&](Hub::Slot& slot) {
@@ -107,8 +111,20 @@ class HubTransport final : public Transport {
       hub_->cv.wait(lock, [&] { return hub_->poisoned || slot->arrived == size(); });
       if (hub_->poisoned) throw TransportError(hub_->reason);
     }
-    copy(*slot);
-    ckc(cudaStreamSynchronize(s), "hub: copies");
+    try {
+      copy(*slot);
+      ckc(cudaStreamSynchronize(s), "hub: copies");
+    } catch (const std::exception& e) {
+      // this rank has arrived: wake the peers blocked on `done` with the same
+      // TransportError instead of leaving them waiting forever
+      std::lock_guard<std::mutex> lock(hub_->mu);
+      if (!hub_->poisoned) {
+        hub_->poisoned = true;
+        hub_->reason = e.what();
+      }
+      hub_->cv.notify_all();
+      throw;
+    }
     std::unique_lock<std::mutex> lock(hub_->mu);
     slot->done++;
     hub_->cv.notify_all();
@@ -191,6 +207,7 @@ class NcclTransport final : public Transport {
   bool capturable() const override { return true; }
   uint64_t bytes_sent() const override { return bytes_; }
   void exchange(cudaStream_t s, const std::vector<Peer>& peers) override {
+    calls++;
     NcclApi& a = nccl();
     ckn(a.GroupStart(), "ncclGroupStart");
     for (const Peer& p : peers) {
@@ -201,10 +218,12 @@ class NcclTransport final : public Transport {
     ckn(a.GroupEnd(), "ncclGroupEnd");
   }
   void allgather(cudaStream_t s, const double* in, double* out, size_t n) override {
+    calls++;
     ckn(nccl().AllGather(in, out, n, ncclDouble, comm_, s), "ncclAllGather");
     bytes_ += n * sizeof(double) * (size_ - 1);
   }
   void gather(cudaStream_t s, const double* in, double* out, size_t n, int root) override {
+    calls++;
     NcclApi& a = nccl();
     ckn(a.GroupStart(), "ncclGroupStart");
     if (rank_ == root) {
@@ -219,6 +238,7 @@ class NcclTransport final : public Transport {
       ckc(cudaMemcpyAsync(out + root * n, in, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "gather self");
   }
   void broadcast(cudaStream_t s, double* buf, size_t n, int root) override {
+    calls++;
     ckn(nccl().Broadcast(buf, buf, n, ncclDouble, root, comm_, s), "ncclBroadcast");
     if (rank_ == root) bytes_ += n * sizeof(double) * (size_ - 1);
   }

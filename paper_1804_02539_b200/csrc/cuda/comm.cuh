@@ -56,6 +56,7 @@ struct Transport {
   virtual void gather(cudaStream_t s, const double* in, double* out, size_t n, int root) = 0;
   virtual void broadcast(cudaStream_t s, double* buf, size_t n, int root) = 0;
   virtual uint64_t bytes_sent() const = 0;
+  uint64_t calls = 0;  // collectives issued (captured ones count once per capture)
 };
 
 // ---- in-process hub shared by the rank threads

@@ -46,6 +46,7 @@ void ck(cudaError_t e, const char* what) {
 struct DevLevel {
   int n = 0, ext = 0, O = 0, K = 0;
   int Ob = 0;  // stored offsets per patch: O, or (O+1)/2 for the symmetric half band
+  int sweep_tw = 0;  // > 0: the band is line-major [K][ext][Ob][tw] (2D line-sweep level)
   long long S = 0, Sp = 0, lat_n = 0, N = 0;
   double* band = nullptr;
   double* sweep_scratch = nullptr;  // line sweep: segment-boundary rows
@@ -111,7 +112,11 @@ struct pmg_ctx {
   int device = 0;
   int dim = 0, degree = 0, K_global = 0, pb = 0, pe = 0, nl = 0;
   int rank = 0, size = 1;
-  std::unique_ptr<Transport> comm;  // null when size == 1
+  // null on a single-GPU context; an NCCL job creates it at any size, so a
+  // world-1 job runs every collective (exchange, all-gathers, coarse
+  // gather / broadcast) through NCCL exactly as a multi-GPU job does
+  std::unique_ptr<Transport> comm;
+  bool multi() const { return comm != nullptr; }
   double* rank_buf = nullptr;       // size doubles (scalar all-gathers)
   double* coarse_parts = nullptr;   // size x n0 (coarse gather on rank 0)
   pmg_cycle_params prm{};
@@ -161,6 +166,27 @@ struct pmg_ctx {
   long long graph_front_launches = 0, graph_back_launches = 0;
   const double* graph_u = nullptr;
   cudaEvent_t ev_norm = nullptr;
+  // device-resident PCG loop: the whole solve is one graph launch, its
+  // iteration body under a WHILE conditional node (one GPU; PMG_HOST_LOOP=1
+  // keeps the host-driven front/back graphs).  Two cached graphs, keyed by
+  // the (f, u) device pointers they were captured on.
+  struct LoopGraph {
+    const double* f = nullptr;
+    const double* u = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    long long head = 0, body = 0;  // kernel launches of the head and of one iteration
+  };
+  LoopGraph loop[2];
+  int loop_next = 0;
+  bool device_loop = true;
+  PcgLoopState* loop_state = nullptr;  // device
+  PcgLoopState* h_loop = nullptr;      // pinned mirror
+  double* loop_hist = nullptr;         // device residual history
+  int loop_hist_cap = 0;
+  // graph-replayed mg_precondition (pmg_precondition), keyed by (r, z)
+  cudaGraphExec_t graph_pre = nullptr;
+  long long graph_pre_launches = 0;
+  const double *graph_pre_r = nullptr, *graph_pre_z = nullptr;
 
   template <class F>
   void capture(cudaGraphExec_t& exec, long long& nlaunch, F&& body) {
@@ -238,6 +264,10 @@ struct pmg_ctx {
     cudaSetDevice(device);
     if (graph_front) cudaGraphExecDestroy(graph_front);
     if (graph_back) cudaGraphExecDestroy(graph_back);
+    if (graph_pre) cudaGraphExecDestroy(graph_pre);
+    for (auto& g : loop)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (h_loop) cudaFreeHost(h_loop);
     if (ev_norm) cudaEventDestroy(ev_norm);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -395,6 +425,7 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
     ck(cudaStreamSynchronize(c.stream), "sweep relayout");
     c.release(L.band, band_n);
     L.band = nb;
+    L.sweep_tw = int(lm / ((long long)L.K * L.ext * L.Ob));
   }
   {
     long long nd = 0, nf = 0;
@@ -442,7 +473,7 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   L.if_comb_src = c.upload(plan.comb_src);
   L.if_tloc = c.alloc<double>(size_t(L.n_iface));
   L.if_t = c.alloc<double>(size_t(L.n_iface));
-  L.if_total = c.size > 1 ? L.if_t : L.if_tloc;
+  L.if_total = c.multi() ? L.if_t : L.if_tloc;
   std::vector<int> send_idx;
   for (const auto& nb : plan.neighbors) send_idx.insert(send_idx.end(), nb.iface.begin(), nb.iface.end());
   L.n_send = L.n_recv = int(send_idx.size());
@@ -793,6 +824,12 @@ void build_ctx(pmg_ctx& c, const pmg_hierarchy_desc& D) {
   c.scal = c.alloc<double>(16);
   ck(cudaMemsetAsync(c.scal, 0, 16 * sizeof(double), c.stream), "memset");
   ck(cudaMallocHost(&c.h_scal, 16 * sizeof(double)), "cudaMallocHost");
+  c.loop_state = c.alloc<PcgLoopState>(1);
+  ck(cudaMallocHost(&c.h_loop, sizeof(PcgLoopState)), "cudaMallocHost");
+  {
+    const char* e = std::getenv("PMG_HOST_LOOP");
+    c.device_loop = !(e && e[0] == '1') && !c.multi();
+  }
   const DevLevel& F = c.lv.back();
   c.staging_n = std::max<long long>(F.N, 1);
   c.staging = c.alloc<double>(size_t(c.staging_n));
@@ -868,12 +905,12 @@ void op_iface_sum(pmg_ctx& c, int l, const double* r) {
   DevLevel& L = c.lv[l];
   launch_iface_partial(c.stream, L.n_iface, L.if_rep_off, L.if_rep_slot, r, L.if_tloc);
   if (L.n_iface) c.launches++;
-  if (c.size > 1) {
+  if (c.multi()) {
     launch_iface_pack(c.stream, L.n_send, L.if_send_idx, L.if_tloc, L.if_send);
     if (L.n_send) c.launches++;
     c.comm->exchange(c.stream, L.peers);
   }
-  if (c.size > 1) {  // on one rank the fold is the identity: totals = if_tloc
+  if (c.multi()) {  // on one rank the fold is the identity: totals = if_tloc
     launch_iface_combine(c.stream, L.n_iface, L.if_comb_off, L.if_comb_src, L.if_tloc, L.if_recv, L.if_t);
     if (L.n_iface) c.launches++;
   }
@@ -893,7 +930,7 @@ void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double
     const char* e = std::getenv("PMG_NO_FUSED_SMOOTH");
     return !(e && e[0] == '1');
   }();
-  if (fused_ok && c.size == 1 && L.int_small && (L.n_face == 0 || L.face_small)) {
+  if (fused_ok && !c.multi() && L.int_small && (L.n_face == 0 || L.face_small)) {
     double flops = 0.0;
     for (int pass = 0; pass < np; ++pass) flops += fd_pass_flops(L, L.int_dims, d, pass);
     TimedScope ts(c, 1, l, flops);
@@ -1078,7 +1115,7 @@ void op_coarse(pmg_ctx& c, const double* r, double* out) {
   TimedScope ts(c, 5, 0, 0.0);
   launch_coarse_gather(c.stream, L.rep_off, L.rep_slot, c.n0, r, c.coarse_rhs);
   c.launches++;
-  if (c.size > 1) {
+  if (c.multi()) {
     c.comm->gather(c.stream, c.coarse_rhs, c.coarse_parts, size_t(c.n0), 0);
     if (c.rank == 0) {
       launch_sum_ranks(c.stream, c.coarse_parts, c.size, c.n0, c.coarse_rhs);
@@ -1089,7 +1126,7 @@ void op_coarse(pmg_ctx& c, const double* r, double* out) {
     launch_coarse_gemv(c.stream, c.Ainv, c.n0, c.coarse_rhs, c.coarse_x);
     c.launches++;
   }
-  if (c.size > 1) c.comm->broadcast(c.stream, c.coarse_x, size_t(c.n0), 0);
+  if (c.multi()) c.comm->broadcast(c.stream, c.coarse_x, size_t(c.n0), 0);
   launch_coarse_scatter(c.stream, L.l2g, L.lat_n, c.coarse_x, out);
   c.launches++;
 }
@@ -1102,7 +1139,7 @@ void op_dot(pmg_ctx& c, int l, const double* a, const double* b, double* dst) {
   launch_dot_partial(c.stream, a, b, L.lat_n, c.partial);
   launch_sum_partials(c.stream, c.partial, dot_blocks(L.lat_n), dst);
   c.launches += 2;
-  if (c.size > 1) {
+  if (c.multi()) {
     c.comm->allgather(c.stream, dst, c.rank_buf, 1);
     launch_sum_ranks(c.stream, c.rank_buf, c.size, 1, dst);
     c.launches++;
@@ -1162,47 +1199,35 @@ void sync_check(pmg_ctx& c) {
   ck(cudaGetLastError(), "kernel launch");
 }
 
-// pcg_generic (multigrid.hpp:155-189) on device-resident vectors f, u.
-int pcg_device(pmg_ctx& c, const double* f, double tol, int max_iter, double* u, double* history, int* iters) {
-  const int Lf = c.nl - 1;
-  const DevLevel& F = c.lv[Lf];
-  const long long n = F.lat_n;
-  double* r = c.pcg_r;
-  double* z = c.pcg_z;
-  double* p = c.pcg_p;
-  double* Ap = c.pcg_Ap;
-  double* racc = c.pcg_acc;
-  double* s = c.scal;
-  launch_fill(c.stream, u, n, 0.0);
-  launch_copy(c.stream, f, r, n);
-  c.launches += 2;
-  auto norm2 = [&]() {  // sqrt(dot(r, accumulate(r)))
+// The PCG iteration pieces shared by the host-driven and the device loop.
+struct PcgParts {
+  pmg_ctx& c;
+  const double* f;
+  double* u;
+  int Lf;
+  long long n;
+  double *r, *z, *p, *Ap, *racc, *s;
+  PcgParts(pmg_ctx& ctx, const double* f_, double* u_)
+      : c(ctx), f(f_), u(u_), Lf(ctx.nl - 1), n(ctx.lv.back().lat_n), r(ctx.pcg_r), z(ctx.pcg_z), p(ctx.pcg_p),
+        Ap(ctx.pcg_Ap), racc(ctx.pcg_acc), s(ctx.scal) {}
+  void norm2() {  // sqrt(dot(r, accumulate(r)))
     op_accumulate(c, Lf, r, racc);
     op_dot(c, Lf, r, racc, s + 5);
     launch_pcg_scalars(c.stream, 2, s);
     c.launches++;
-  };
-  auto read_scalars = [&]() {
-    ck(cudaMemcpyAsync(c.h_scal, s, 8 * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "scalar D2H");
-    sync_check(c);
-  };
-  norm2();
-  read_scalars();
-  const double r0 = c.h_scal[6];
-  history[0] = r0;
-  *iters = 0;
-  if (r0 == 0.0) return PMG_OK;
-  launch_fill(c.stream, z, n, 0.0);
-  c.launches++;
-  precondition(c, r, z);
-  launch_copy(c.stream, z, p, n);
-  c.launches++;
-  op_dot(c, Lf, r, z, s + 0);  // rz
-  // iteration front: Ap, alpha, u += alpha p, r -= alpha Ap, |r| -> host
-  auto front = [&]() {
+  }
+  void start() {  // u = 0, r = f, |r0|
+    launch_fill(c.stream, u, n, 0.0);
+    launch_copy(c.stream, f, r, n);
+    c.launches += 2;
+    norm2();
+  }
+  // iteration front: Ap, alpha, u += alpha p, r -= alpha Ap, |r|
+  void front() {
+    const DevLevel& F = c.lv[Lf];
     op_spmv(c, Lf, p, nullptr, Ap, c.partial);  // Ap and the partials of Ap.p
     launch_sum_partials(c.stream, c.partial, spmv_partials(c.dim, c.degree, F.S, F.K, F.Ob != F.O, c.sweep), s + 1);
-    if (c.size > 1) {  // pAp over all ranks, ascending rank order
+    if (c.multi()) {  // pAp over all ranks, ascending rank order
       c.comm->allgather(c.stream, s + 1, c.rank_buf, 1);
       launch_sum_ranks(c.stream, c.rank_buf, c.size, 1, s + 1);
       c.launches++;
@@ -1212,17 +1237,45 @@ int pcg_device(pmg_ctx& c, const double* f, double tol, int max_iter, double* u,
     launch_axpy(c.stream, 0.0, s + 2, -1.0, Ap, r, n);
     c.launches += 4;
     norm2();
-    ck(cudaMemcpyAsync(c.h_scal, s, 8 * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "scalar D2H");
-  };
-  // iteration back: z = M r, beta, p = z + beta p.  Enqueued before the host
-  // has seen |r|; after the last iteration it only touches z and p.
-  auto back = [&]() {
+  }
+  // iteration back: z = M r, beta, p = z + beta p
+  void back() {
     precondition(c, r, z);
     op_dot(c, Lf, r, z, s + 3);          // rz_next
     launch_pcg_scalars(c.stream, 1, s);  // beta, rz = rz_next
     launch_xpay(c.stream, z, 0.0, s + 4, p, n);
     c.launches += 2;
+  }
+};
+
+// pcg_generic (multigrid.hpp:155-189) driven from the host: two graphs per
+// iteration (front, back); the back half is enqueued before the host has
+// seen |r|, so after the last iteration one V-cycle is computed and dropped.
+// Multi-rank contexts and PMG_HOST_LOOP=1 take this path.
+int pcg_host_loop(pmg_ctx& c, const double* f, double tol, int max_iter, double* u, double* history, int* iters) {
+  PcgParts P(c, f, u);
+  double* s = c.scal;
+  auto read_scalars = [&]() {
+    ck(cudaMemcpyAsync(c.h_scal, s, 8 * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "scalar D2H");
+    sync_check(c);
   };
+  P.start();
+  read_scalars();
+  const double r0 = c.h_scal[6];
+  history[0] = r0;
+  *iters = 0;
+  if (r0 == 0.0) return PMG_OK;
+  launch_fill(c.stream, P.z, P.n, 0.0);
+  c.launches++;
+  precondition(c, P.r, P.z);
+  launch_copy(c.stream, P.z, P.p, P.n);
+  c.launches++;
+  op_dot(c, P.Lf, P.r, P.z, s + 0);  // rz
+  auto front = [&]() {
+    P.front();
+    ck(cudaMemcpyAsync(c.h_scal, s, 8 * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "scalar D2H");
+  };
+  auto back = [&]() { P.back(); };
   const bool graphs = c.use_graphs && !c.profiling;
   if (graphs && c.graph_u != u) {
     c.capture(c.graph_front, c.graph_front_launches, front);
@@ -1236,12 +1289,10 @@ int pcg_device(pmg_ctx& c, const double* f, double tol, int max_iter, double* u,
       front();
     }
     ck(cudaEventRecord(c.ev_norm, c.stream), "cudaEventRecord");
-    if (k < max_iter) {
-      if (graphs)
-        c.launch_graph(c.graph_back, c.graph_back_launches);
-      else
-        back();
-    }
+    // with graphs the back half is enqueued speculatively (the GPU never
+    // waits for the host); direct launches (profiling) stop exactly as
+    // pcg_generic does, so an instrumented solve runs the device loop's kernels
+    if (graphs && k < max_iter) c.launch_graph(c.graph_back, c.graph_back_launches);
     ck(cudaEventSynchronize(c.ev_norm), "cudaEventSynchronize");
     if (c.h_scal[7] != 0.0) {
       c.h_scal[7] = 0.0;
@@ -1253,8 +1304,128 @@ int pcg_device(pmg_ctx& c, const double* f, double tol, int max_iter, double* u,
     history[k] = rn;
     *iters = k;
     if (rn <= tol * r0) return PMG_OK;
+    if (!graphs && k < max_iter) back();
   }
   return PMG_ERR_DIVERGENCE;
+}
+
+// Capture the whole solve as one graph: head (u = 0, r = f, |r0|, loop
+// condition, z = p = 0, rz = +inf) and a WHILE node whose body is one PCG
+// iteration in the order back, front, check.  With rz = +inf the first
+// body's beta is 0 and p = z + 0 p = z exactly, and its rz = r.z is the same
+// dot as the host loop's, so both loops produce the same bits.
+void capture_loop(pmg_ctx& c, pmg_ctx::LoopGraph& g, const double* f, double* u) {
+  if (g.exec) {
+    cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+  }
+  g.f = g.u = nullptr;
+  PcgParts P(c, f, u);
+  cudaGraph_t graph = nullptr;
+  ck(cudaGraphCreate(&graph, 0), "cudaGraphCreate");
+  cudaStream_t saved = c.stream;
+  const long long before = c.launches;
+  bool capturing = false;
+  try {
+    cudaGraphConditionalHandle handle;
+    ck(cudaGraphConditionalHandleCreate(&handle, graph, 0, cudaGraphCondAssignDefault), "conditional handle");
+    c.stream = c.own_stream;
+    ck(cudaStreamBeginCaptureToGraph(c.own_stream, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
+       "capture head");
+    capturing = true;
+    P.start();
+    launch_pcg_check(c.stream, 1, c.loop_state, c.scal, c.loop_hist, handle);
+    launch_fill(c.stream, P.z, P.n, 0.0);
+    launch_fill(c.stream, P.p, P.n, 0.0);
+    c.launches += 3;
+    cudaStreamCaptureStatus st;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    ck(cudaStreamGetCaptureInfo(c.own_stream, &st, nullptr, nullptr, &deps, &ndeps), "capture info");
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    ck(cudaGraphAddNode(&cnode, graph, deps, ndeps, &cp), "while node");
+    ck(cudaStreamUpdateCaptureDependencies(c.own_stream, &cnode, 1, cudaStreamSetCaptureDependencies),
+       "capture dependencies");
+    cudaGraph_t tmp = nullptr;
+    capturing = false;
+    ck(cudaStreamEndCapture(c.own_stream, &tmp), "end capture head");
+    g.head = c.launches - before;
+    const long long mid = c.launches;
+    ck(cudaStreamBeginCaptureToGraph(c.own_stream, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal),
+       "capture body");
+    capturing = true;
+    P.back();
+    P.front();
+    launch_pcg_check(c.stream, 0, c.loop_state, c.scal, c.loop_hist, handle);
+    c.launches++;
+    capturing = false;
+    ck(cudaStreamEndCapture(c.own_stream, &tmp), "end capture body");
+    g.body = c.launches - mid;
+    ck(cudaGraphInstantiate(&g.exec, graph, 0), "instantiate loop graph");
+  } catch (...) {
+    if (capturing) {
+      cudaGraph_t tmp = nullptr;
+      cudaStreamEndCapture(c.own_stream, &tmp);
+    }
+    cudaGraphDestroy(graph);
+    c.stream = saved;
+    c.launches = before;
+    throw;
+  }
+  cudaGraphDestroy(graph);
+  c.stream = saved;
+  c.launches = before;
+  g.f = f;
+  g.u = u;
+}
+
+int pcg_device_loop(pmg_ctx& c, const double* f, double tol, int max_iter, double* u, double* history, int* iters) {
+  if (c.loop_hist_cap < max_iter + 1) {  // the history buffer is baked into the graphs
+    const int cap = std::max(max_iter + 1, 501);
+    if (c.loop_hist) c.release(c.loop_hist, size_t(c.loop_hist_cap));
+    c.loop_hist = c.alloc<double>(size_t(cap));
+    c.loop_hist_cap = cap;
+    for (auto& g : c.loop) g.f = g.u = nullptr;
+  }
+  pmg_ctx::LoopGraph* g = nullptr;
+  for (auto& cand : c.loop)
+    if (cand.exec && cand.f == f && cand.u == u) g = &cand;
+  if (!g) {
+    g = &c.loop[c.loop_next];
+    c.loop_next ^= 1;
+    capture_loop(c, *g, f, u);
+  }
+  c.h_loop->k = 0;
+  c.h_loop->status = 0;
+  c.h_loop->max_iter = max_iter;
+  c.h_loop->tol = tol;
+  c.h_loop->r0 = 0.0;
+  ck(cudaMemcpyAsync(c.loop_state, c.h_loop, sizeof(PcgLoopState), cudaMemcpyHostToDevice, c.stream), "state H2D");
+  ck(cudaGraphLaunch(g->exec, c.stream), "cudaGraphLaunch");
+  ck(cudaMemcpyAsync(c.h_loop, c.loop_state, sizeof(PcgLoopState), cudaMemcpyDeviceToHost, c.stream), "state D2H");
+  sync_check(c);
+  const int k = c.h_loop->k;
+  ck(cudaMemcpy(history, c.loop_hist, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost), "history D2H");
+  c.launches += g->head + (long long)k * g->body;
+  *iters = k;
+  switch (c.h_loop->status) {
+    case 1: return PMG_OK;
+    case 2: throw PmgError(PMG_ERR_DEFINITENESS, "pcg: search direction with nonpositive energy");
+    case 3: return PMG_ERR_DIVERGENCE;
+    default: throw PmgError(PMG_ERR_GENERIC, "pcg: device loop ended without a decision");
+  }
+}
+
+int pcg_device(pmg_ctx& c, const double* f, double tol, int max_iter, double* u, double* history, int* iters) {
+  if (c.device_loop && c.use_graphs && !c.profiling)
+    return pcg_device_loop(c, f, tol, max_iter, u, history, iters);
+  return pcg_host_loop(c, f, tol, max_iter, u, history, iters);
 }
 
 template <class F>
@@ -1269,6 +1440,9 @@ int guarded(pmg_ctx* c, F&& f) {
   } catch (const TransportFailure& e) {
     if (c) c->err = e.what();
     return PMG_ERR_TRANSPORT;
+  } catch (const LaunchError& e) {
+    if (c) c->err = e.what();
+    return PMG_ERR_CUDA;
   } catch (const std::exception& e) {
     if (c) c->err = e.what();
     return PMG_ERR_GENERIC;
@@ -1317,7 +1491,7 @@ int pmg_ctx_create(const pmg_hierarchy_desc* desc, int device, const pmg_comm_de
       c->size = comm->size;
       c->pb = comm->patch_begin;
       c->pe = comm->patch_end;
-      if (comm->size > 1) {
+      if (comm->size > 1 || comm->transport == PMG_TRANSPORT_NCCL) {
         if (comm->transport == PMG_TRANSPORT_NCCL) {
           c->comm = make_nccl_transport(comm->nccl_id, comm->rank, comm->size);
         } else if (comm->transport == PMG_TRANSPORT_HUB) {
@@ -1397,8 +1571,36 @@ int pmg_ctx_info(pmg_ctx* ctx, int what, int64_t* out) {
       case 3: *out = ctx->lv[level].N; break;
       case 4: *out = ctx->pe - ctx->pb; break;
       case 5: *out = int64_t(ctx->assembly_seconds * 1e6); break;
+      case 6: *out = ctx->comm ? int64_t(ctx->comm->calls) : 0; break;
       default: throw PmgError(PMG_ERR_CONFIG, "unknown info query");
     }
+  });
+}
+
+int pmg_band_download(pmg_ctx* ctx, int level, double* host, int64_t n) {
+  return guarded(ctx, [&] {
+    need(level >= 0 && level < ctx->nl, PMG_ERR_DOMAIN, "level out of range");
+    const DevLevel& L = ctx->lv[level];
+    const size_t per = size_t(L.O) * size_t(L.S);
+    need(host != nullptr && n == int64_t(per) * L.K, PMG_ERR_DOMAIN,
+         "band download: n must be local patches x (2p+1)^d x (n+p)^d");
+    double* tmp = nullptr;
+    ck(cudaMalloc(&tmp, per * sizeof(double)), "cudaMalloc band expand");
+    try {
+      for (int k = 0; k < L.K; ++k) {
+        const double* src = L.sweep_tw > 0 ? L.band + size_t(k) * L.ext * L.Ob * L.sweep_tw
+                                           : L.band + size_t(k) * L.Ob * L.Sp;
+        launch_band_expand(ctx->stream, ctx->dim, ctx->degree, L.ext, L.S, L.Ob, L.Sp, L.sweep_tw, src, tmp);
+        ck(cudaGetLastError(), "band expand");
+        ck(cudaMemcpyAsync(host + size_t(k) * per, tmp, per * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream),
+           "band download");
+        ck(cudaStreamSynchronize(ctx->stream), "band download");
+      }
+    } catch (...) {
+      cudaFree(tmp);
+      throw;
+    }
+    ck(cudaFree(tmp), "cudaFree");
   });
 }
 
@@ -1597,9 +1799,21 @@ int pmg_precondition(pmg_ctx* ctx, const pmg_vec* r, pmg_vec* z) {
     check_vec(ctx, r, ctx->nl - 1);
     check_vec(ctx, z, ctx->nl - 1);
     need(r->d != z->d, PMG_ERR_DOMAIN, "precondition: input and output must differ");
-    launch_fill(ctx->stream, z->d, z->n, 0.0);
-    ctx->launches++;
-    precondition(*ctx, r->d, z->d);
+    auto body = [&]() {
+      launch_fill(ctx->stream, z->d, z->n, 0.0);
+      ctx->launches++;
+      precondition(*ctx, r->d, z->d);
+    };
+    if (ctx->use_graphs && !ctx->profiling) {  // one graph launch per V-cycle, cached by (r, z)
+      if (!ctx->graph_pre || ctx->graph_pre_r != r->d || ctx->graph_pre_z != z->d) {
+        ctx->capture(ctx->graph_pre, ctx->graph_pre_launches, body);
+        ctx->graph_pre_r = r->d;
+        ctx->graph_pre_z = z->d;
+      }
+      ctx->launch_graph(ctx->graph_pre, ctx->graph_pre_launches);
+    } else {
+      body();
+    }
   });
 }
 

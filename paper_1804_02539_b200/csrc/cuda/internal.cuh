@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -43,6 +45,12 @@ constexpr int kThreads = 256;
 
 bool pdl_enabled();
 
+// A failed launch (configuration, shared memory, ...) is an error of the call
+// that issued it: launch_k throws, the C ABI maps it to PMG_ERR_CUDA.
+struct LaunchError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   static_assert(sizeof...(KArgs) == sizeof...(Args), "kernel argument count");
@@ -56,7 +64,27 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) throw LaunchError(std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+// Raise `kernel`'s dynamic shared-memory limit to `bytes` on the CURRENT
+// device.  Function attributes belong to each device's context, so the record
+// is keyed by (kernel, device); hub ranks on several devices of one process
+// and concurrent rank threads are both safe.  Throws LaunchError on failure.
+inline void ensure_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) throw LaunchError(std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+  std::lock_guard<std::mutex> g(mu);
+  size_t& have = done[{kernel, dev}];
+  if (have >= bytes) return;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e != cudaSuccess)
+    throw LaunchError(std::string("cudaFuncSetAttribute(MaxDynamicSharedMemorySize): ") + cudaGetErrorString(e));
+  have = bytes;
 }
 
 // ---------------------------------------------------------------- assembly
@@ -143,6 +171,32 @@ void spmv_sweep_scratch(int dim, int degree, int ext, long long S, int K, bool h
                         long long* flags);
 void launch_sweep_relayout(cudaStream_t s, int degree, int ext, long long S, int K, long long Sp, const double* src,
                            double* dst);
+// One patch's device band (offset-major [Ob][Sp], or line-major [ext][Ob][tw]
+// when tw > 0) expanded to the reference's index-free full band [O][S]
+// (offset o = sum_a (delta_a + p) (2p+1)^a, axis 0 fastest): stored offsets
+// are copied, the upper half of a symmetric half band is the mirrored lower
+// entry A(r, r+s) = A(r+s, r).  Pairs outside the lattice read 0.
+void launch_band_expand(cudaStream_t s, int dim, int degree, int ext, long long S, int Ob, long long Sp, int tw,
+                        const double* band_patch, double* full);
+
+// ---------------------------------------------------------------- device PCG loop
+// State of a device-resident pcg_generic loop (multigrid.hpp:155-189): the
+// iteration counter, the stopping decision and the residual norms stay on the
+// device; a WHILE conditional graph node repeats the iteration body until
+// pcg_check clears the condition.
+struct PcgLoopState {
+  int k;         // iterations done
+  int status;    // 0 running, 1 converged, 2 non-positive energy, 3 iteration cap
+  int max_iter;  // set by the host before each launch
+  int pad;
+  double tol;    // set by the host before each launch
+  double r0;
+};
+// first != 0: history[0] = |r0| and the loop condition (|r0| != 0), and
+// scal[0] = +inf so the first body's beta = rz / inf = 0 gives p = z exactly;
+// else: history[++k] = |r_k| and the stop test (definiteness flag, tol, cap)
+void launch_pcg_check(cudaStream_t s, int first, PcgLoopState* st, double* scal, double* history,
+                      cudaGraphConditionalHandle handle);
 
 // ---------------------------------------------------------------- misc kernels
 void launch_fill(cudaStream_t s, double* x, long long n, double v);

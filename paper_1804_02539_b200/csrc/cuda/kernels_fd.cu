@@ -493,10 +493,9 @@ void launch_smooth_small(cudaStream_t s, const SmoothSmallArgs& a, size_t smem) 
 }
 
 void fd_configure() {
-  cudaFuncSetAttribute(fd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(smooth_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-#define PMG_FD_ATTR(NT, W) \
-  cudaFuncSetAttribute(fd_pass_dmma_kernel<NT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FdTile<NT, W>::smem));
+  ensure_smem((const void*)fd_small_kernel, 200 * 1024);
+  ensure_smem((const void*)smooth_small_kernel, 200 * 1024);
+#define PMG_FD_ATTR(NT, W) ensure_smem((const void*)fd_pass_dmma_kernel<NT, W>, FdTile<NT, W>::smem);
   PMG_FD_ATTR(3, 1) PMG_FD_ATTR(5, 1) PMG_FD_ATTR(9, 1) PMG_FD_ATTR(11, 1) PMG_FD_ATTR(3, 2) PMG_FD_ATTR(5, 2)
   PMG_FD_ATTR(9, 2) PMG_FD_ATTR(11, 2)
 #undef PMG_FD_ATTR

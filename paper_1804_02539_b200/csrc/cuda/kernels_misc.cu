@@ -515,7 +515,43 @@ __global__ void pcg_scalars_kernel(int op, double* s) {
   }
 }
 
+__global__ void pcg_check_kernel(int first, PcgLoopState* st, double* s, double* hist,
+                                 cudaGraphConditionalHandle handle) {
+  PMG_PDL_ENTRY();
+  if (threadIdx.x != 0) return;
+  unsigned go = 0;
+  if (first) {
+    const double r0 = s[6];
+    st->r0 = r0;
+    st->k = 0;
+    hist[0] = r0;
+    st->status = r0 == 0.0 ? 1 : 0;  // pcg_generic returns at once on a zero residual
+    s[0] = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    go = r0 != 0.0;
+  } else {
+    const int k = ++st->k;
+    const double rn = s[6];
+    hist[k] = rn;
+    if (s[7] != 0.0) {  // pAp <= 0 (DefinitenessError, multigrid.hpp:176)
+      s[7] = 0.0;
+      st->status = 2;
+    } else if (rn <= st->tol * st->r0) {  // multigrid.hpp:182
+      st->status = 1;
+    } else if (k >= st->max_iter) {  // DivergenceError, multigrid.hpp:188
+      st->status = 3;
+    } else {
+      go = 1;
+    }
+  }
+  cudaGraphSetConditional(handle, go);
+}
+
 }  // namespace
+
+void launch_pcg_check(cudaStream_t s, int first, PcgLoopState* st, double* scal, double* history,
+                      cudaGraphConditionalHandle handle) {
+  launch_k(pcg_check_kernel, dim3(1), dim3(32), 0, s, first, st, scal, history, handle);
+}
 
 bool pdl_enabled() {
   static const bool on = [] {

@@ -836,20 +836,12 @@ void launch_tma(cudaStream_t s, const SpmvArgs& a) {
   const long long grid = (a.S + kRowsTma - 1) / kRowsTma * a.K;
   if (a.half) {
     const size_t smem = (size_t)kStages * (W * kSeg + (kHalfXWindow ? XWindow<P>::kLen : 0)) * sizeof(double);
-    static bool configured = false;  // per process; one device per context thread
-    if (!configured) {
-      cudaFuncSetAttribute(spmv_tma_half_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      configured = true;
-    }
+    ensure_smem((const void*)spmv_tma_half_kernel<D, P>, smem);
     launch_k(spmv_tma_half_kernel<D, P>, dim3(unsigned(grid)), dim3(kRowsTma + 32), smem, s, a);
     return;
   }
   const size_t smem = (size_t)kStages * W * kRowsTma * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(spmv_tma_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = true;
-  }
+  ensure_smem((const void*)spmv_tma_kernel<D, P>, smem);
   launch_k(spmv_tma_kernel<D, P>, dim3(unsigned(grid)), dim3(kRowsTma + 32), smem, s, a);
 }
 
@@ -915,11 +907,7 @@ static bool sweep_cfg(int dim, int degree, int ext, long long S, int K, bool hal
 
 template <int P>
 void launch_sweep(cudaStream_t s, const SpmvArgs& a, const SweepCfg& g, size_t smem) {
-  static size_t configured = 0;  // per process; one device per context thread
-  if (smem > configured) {
-    cudaFuncSetAttribute(spmv_sweep2d_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = smem;
-  }
+  ensure_smem((const void*)spmv_sweep2d_kernel<P>, smem);
   launch_k(spmv_sweep2d_kernel<P>, dim3(unsigned(g.segs * a.K)), dim3(g.nc + 32), smem, s, a, g);
 }
 
@@ -955,6 +943,50 @@ int spmv_stored_offsets(int dim, int degree, long long S, bool allow_half) {
 }
 
 int spmv_blocks(long long rows) { return int((rows + kThreads - 1) / kThreads); }
+
+namespace {
+__global__ void band_expand_kernel(const double* __restrict__ band, double* __restrict__ full, int dim, int p,
+                                   int ext, long long S, int O, int Ob, long long Sp, int tw) {
+  const int W = 2 * p + 1;
+  const int padl = (p + 1) & ~1;
+  const long long n = (long long)O * S;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int o = int(e / S);
+    const long long r = e % S;
+    int ob = o;
+    long long row = r;
+    if (o >= Ob) {  // upper half of a symmetric half band: mirror offset, shifted row
+      long long shift = 0, mul = 1;
+      int t = o;
+      for (int a = 0; a < dim; ++a) {
+        shift += (long long)(t % W - p) * mul;
+        t /= W;
+        mul *= ext;
+      }
+      ob = O - 1 - o;
+      row = r + shift;
+    }
+    double v = 0.0;
+    if (row >= 0 && row < S) {
+      if (tw > 0) {
+        const long long L = row / ext;
+        const int i = int(row % ext);
+        v = band[(L * Ob + ob) * tw + padl + i];
+      } else {
+        v = band[(long long)ob * Sp + row];
+      }
+    }
+    full[e] = v;
+  }
+}
+}  // namespace
+
+void launch_band_expand(cudaStream_t s, int dim, int degree, int ext, long long S, int Ob, long long Sp, int tw,
+                        const double* band_patch, double* full) {
+  const int W = 2 * degree + 1;
+  const int O = dim == 2 ? W * W : W * W * W;
+  band_expand_kernel<<<148 * 8, 256, 0, s>>>(band_patch, full, dim, degree, ext, S, O, Ob, Sp, tw);
+}
 
 long long spmv_sweep_band_doubles(int dim, int degree, int ext, long long S, int K, bool half, int sweep) {
   SweepCfg g;

@@ -1,5 +1,6 @@
-// C++ drop-in demonstration: the reference's pcg_generic / mg_precondition
-// templates (restated in include/patchmg_gpu.hpp) driving GpuBackend through
+// C++ drop-in demonstration without the reference's headers: the restated
+// pcg_generic / mg_precondition templates (include/patchmg_gpu.hpp, namespace
+// patchmg_gpu::generic) driving GpuBackend through
 // the C ABI, next to the device-resident fused solve.  Prints one JSON line.
 //   pcg_cpp <domain> <degree> <levels> <n0>
 #include <algorithm>
@@ -33,8 +34,8 @@ int main(int argc, char** argv) {
     const int L = b.finest_level();
     auto fd = b.to_distributed_owner(L, f);
     std::vector<double> hist;
-    auto u = patchmg_gpu::pcg_generic(
-        b, fd, 1e-8, 500, [&](const patchmg_gpu::GpuBackend::DistVec& r) { return patchmg_gpu::mg_precondition(b, r); },
+    auto u = patchmg_gpu::generic::pcg_generic(
+        b, fd, 1e-8, 500, [&](const patchmg_gpu::GpuBackend::DistVec& r) { return patchmg_gpu::generic::mg_precondition(b, r); },
         hist);
     std::vector<double> ug = b.gather_global(L, u, n);
     std::vector<double> u2(size_t(n), 0.0), hist2(501, 0.0);

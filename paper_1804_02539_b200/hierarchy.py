@@ -107,6 +107,25 @@ class Hierarchy:
         return np.ctypeslib.as_array(self.desc.levels[level].band, shape=(self.num_patches * o * s,)).reshape(
             self.num_patches, o, s)
 
+    def adopt_device_bands(self, backend) -> float:
+        """Give the levels assembled on the device (PMG_BAND_ASSEMBLE) host bands
+        downloaded from `backend` (a single-GPU GpuBackend built on this
+        hierarchy), so host consumers -- the CPU oracle and baseline -- read
+        exactly the operator the device applies.  Returns seconds spent."""
+        import time
+        t = time.perf_counter()
+        self._adopted = getattr(self, "_adopted", {})
+        for level in range(self.num_levels):
+            ld = self.desc.levels[level]
+            if ld.band_format != N.PMG_BAND_ASSEMBLE:
+                continue
+            band = np.ascontiguousarray(backend.download_band(level))
+            self._adopted[level] = band
+            ld.band = band.ctypes.data_as(N._dp)
+            ld.band_format = N.PMG_BAND_TENSOR
+        self.assembly = "device (bands downloaded to the host)"
+        return time.perf_counter() - t
+
     def pieces(self, level: int):
         ld = self.desc.levels[level]
         return [ld.pieces[i] for i in range(ld.num_pieces)]

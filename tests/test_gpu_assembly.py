@@ -55,3 +55,29 @@ def test_pcg_on_device_assembled_hierarchy(dom, p, lv, n0):
     u, rep = GpuBackend(hd).pcg_solve(f)
     assert rep.iterations == len(hist_ref) - 1
     assert rel(u, u_ref) < 1e-10
+
+
+@pytest.mark.parametrize("dom,p,lv,n0,env", [
+    ("c2", 4, 5, 2, {}), ("c2", 4, 5, 2, {"PMG_SWEEP_MIN_EXT": "1"}),  # offset-major and line-major levels
+    ("c2", 4, 4, 2, {"PMG_FULL_BAND": "1"}), ("c4", 3, 3, 2, {}), ("c3", 8, 3, 2, {}), ("fichera", 2, 3, 1, {})])
+def test_band_download_feeds_the_oracle(dom, p, lv, n0, env, monkeypatch):
+    """pmg_band_download: a device-assembled hierarchy hands its bands to the
+    host (Hierarchy.adopt_device_bands); the oracle on those bands applies the
+    host-assembled operator to 1e-13 on every level and its PCG matches the
+    GPU's iteration count and solution."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    hh = Hierarchy(dom, p, lv, n0=n0)
+    hd = Hierarchy(dom, p, lv, n0=n0, assembly="device")
+    bd = GpuBackend(hd)
+    hd.adopt_device_bands(bd)
+    od, oh = oracle.Oracle(hd), oracle.Oracle(hh)
+    rng = np.random.default_rng(9)
+    for level in range(hh.num_levels):
+        u = rng.uniform(-1.0, 1.0, hh.num_dofs(level))
+        assert rel(od.apply_op(level, u), oh.apply_op(level, u)) < 1e-13, level
+    f = hd.rhs()
+    u_ref, hist_ref, _, _ = od.pcg_solve(f)
+    u, rep = bd.pcg_solve(f)
+    assert rep.iterations == len(hist_ref) - 1
+    assert rel(u, u_ref) < 1e-10

@@ -243,3 +243,59 @@ def test_line_sweep_matches_tma_half(dom, p, lv, n0, min_ext, monkeypatch):
         assert rel(out["1"][0][level][1], ref.residual(level, f, u)) < 1e-13
     assert out["1"][2] == out["0"][2]
     assert rel(out["1"][1], out["0"][1]) < 1e-10
+
+
+@pytest.mark.parametrize("ntc", ["3", "5", "9", "11"])
+@pytest.mark.parametrize("dom,p,lv,n0", [("c2", 4, 5, 2), ("c4", 3, 3, 2), ("c3", 8, 5, 2), ("c1", 2, 6, 2)])
+def test_smooth_forced_fd_panels(dom, p, lv, n0, ntc, monkeypatch):
+    """Every fast-diagonalization column panel (fd_pass_dmma_kernel<NTC, 1>,
+    NTC = 3, 5, 9, 11 n-tiles of 8 columns; fd_pick_ntc chooses per level)
+    against the oracle's FastDiagonalSolver::solve path (tensor.cpp:132-140)
+    on every level; the bench's c2 finest level runs NTC = 9."""
+    monkeypatch.setenv("PMG_FD_NTC", ntc)
+    h = Hierarchy(dom, p, lv, n0=n0)
+    b, o = GpuBackend(h), oracle.Oracle(h)
+    for level in range(h.num_levels):
+        r = rand(h.num_dofs(level), 61 + level)
+        got = b.gather_global(level, b.smooth(level, b.to_distributed_owner(level, r)))
+        assert rel(got, o.smooth(level, r)) < 1e-12, level
+    f = h.rhs()
+    u_ref, hist_ref, _, _ = o.pcg_solve(f)
+    u, rep = b.pcg_solve(f)
+    assert rep.iterations == len(hist_ref) - 1
+    assert rel(u, u_ref) < 1e-10
+
+
+@pytest.mark.parametrize("dom,p,lv,n0", [("c2", 4, 5, 2), ("c4", 3, 3, 2), ("lshape", 2, 3, 1), ("c2", 4, 7, 2)])
+def test_device_loop_matches_host_loop(dom, p, lv, n0, monkeypatch):
+    """The device-resident PCG loop (one graph launch per solve, the iteration
+    body under a WHILE conditional node, the stop test on the device) against
+    the host-driven front/back graphs (PMG_HOST_LOOP=1): the same bits in u
+    and in every residual norm, the same iteration count, the reference's
+    error behaviour at the iteration cap (DivergenceError, multigrid.hpp:188)
+    and on a zero load vector (no iteration, multigrid.hpp:163-164)."""
+    from paper_1804_02539_b200.errors import DivergenceError
+    h = Hierarchy(dom, p, lv, n0=n0)
+    f = h.rhs()
+    b = GpuBackend(h)
+    u1, rep1 = b.pcg_solve(f)
+    u1b, rep1b = b.pcg_solve(f)  # cached graph
+    monkeypatch.setenv("PMG_HOST_LOOP", "1")
+    b2 = GpuBackend(h)
+    u2, rep2 = b2.pcg_solve(f)
+    assert rep1.iterations == rep2.iterations == rep1b.iterations
+    assert np.array_equal(u1, u2) and np.array_equal(u1, u1b)
+    assert np.array_equal(np.array(rep1.residual_history), np.array(rep2.residual_history))
+    # device vectors through pcg_solve_device (a second cached graph) agree too
+    L = h.finest_level
+    ud, repd = b.pcg_solve_device(b.to_distributed_owner(L, f))
+    assert repd.iterations == rep1.iterations
+    assert np.array_equal(b.gather_global(L, ud), u1)
+    for bb in (b, b2):
+        with pytest.raises(DivergenceError):
+            bb.pcg_solve(f, max_iter=3)
+        uz, repz = bb.pcg_solve(np.zeros_like(f))
+        assert repz.iterations == 0 and not uz.any()
+    # and the solve still works after the error paths
+    u3, rep3 = b.pcg_solve(f)
+    assert np.array_equal(u3, u1)

@@ -259,3 +259,25 @@ def test_parallel_iterations_track_serial():  # test_parallel.cpp:581-625
             assert np.all(np.abs(hp[:k] - hs[:k]) <= 1e-10 * hs[:k])
     _, again, _, _ = o.pcg_solve(f, ranks=4)
     assert np.array_equal(again, r4)
+
+
+def test_oracle_coarse_modes_agree_to_conditioning():
+    """The oracle's second exact coarse solver (explicit inverse, the CUDA
+    path's choice) against its LLT substitution (Hierarchy::coarse_solve,
+    multigrid.cpp:52-55): equal to kappa(A_0) eps, same PCG iterations."""
+    import numpy as np
+    import oracle
+    from paper_1804_02539_b200 import Hierarchy
+    h = Hierarchy("c3", 4, 2, n0=2)
+    o = oracle.Oracle(h)
+    r = np.random.default_rng(1).uniform(-1, 1, h.num_dofs(0))
+    x0 = o.coarse_solve(r)
+    o.set_coarse_mode(1)
+    x1 = o.coarse_solve(r)
+    kappa = np.linalg.cond(h.coarse_matrix())
+    assert np.abs(x1 - x0).max() <= 10 * kappa * np.finfo(float).eps * np.abs(x0).max()
+    f = h.rhs()
+    _, h1, _, _ = o.pcg_solve(f)
+    o.set_coarse_mode(0)
+    _, h0, _, _ = o.pcg_solve(f)
+    assert len(h1) == len(h0)
