@@ -365,7 +365,11 @@ def main():
         b = RankBackend(h, rank, world, local)
     else:
         b = GpuBackend(h, device=local)
-    stream = torch.cuda.current_stream()
+    # a dedicated stream: every launch of the library and every timing event
+    # go to it (the legacy default stream would not order against the
+    # library's non-blocking streams)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     b.set_stream(stream.cuda_stream)
     f_host = h.rhs()
     f_dev = b.to_distributed_owner(L, f_host)

@@ -47,6 +47,7 @@ struct DevLevel {
   int n = 0, ext = 0, O = 0, K = 0;
   int Ob = 0;  // stored offsets per patch: O, or (O+1)/2 for the symmetric half band
   int sweep_tw = 0;  // > 0: the band is line-major [K][ext][Ob][tw] (2D line-sweep level)
+  int sweep3_front = 0, sweep3_e2p = 0;  // e2p > 0: plane-major [K][ext][Ob][e2p] (3D plane-sweep level)
   long long S = 0, Sp = 0, lat_n = 0, N = 0;
   double* band = nullptr;
   double* sweep_scratch = nullptr;  // line sweep: segment-boundary rows
@@ -131,6 +132,7 @@ struct pmg_ctx {
   double* partial = nullptr;
   int partial_n = 0;
   int sweep = 128;  // 2D line-sweep SpMV on lines of >= sweep rows; 0: off (PMG_SWEEP, PMG_SWEEP_MIN_EXT at creation)
+  int sweep3 = 30;  // 3D plane-sweep SpMV on lattices of >= sweep3 rows per axis; 0: off (PMG_SWEEP3D)
   double* scal = nullptr;     // device scalars
   double* h_scal = nullptr;   // pinned mirror
   double* staging = nullptr;  // device global-vector staging (finest num_dofs)
@@ -417,6 +419,9 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
     const char* e = std::getenv("PMG_SWEEP");
     const char* m = std::getenv("PMG_SWEEP_MIN_EXT");
     c.sweep = (e && e[0] == '0') ? 0 : std::max(1, m ? std::atoi(m) : 128);
+    // 3D plane sweep on lattices with >= PMG_SWEEP3D rows per axis (default 30; 0 disables)
+    const char* e3 = std::getenv("PMG_SWEEP3D");
+    c.sweep3 = (e && e[0] == '0') ? 0 : (e3 ? std::atoi(e3) : 30);
   }
   if (const long long lm = spmv_sweep_band_doubles(d, p, L.ext, S, L.K, L.Ob != L.O, c.sweep)) {
     double* nb = c.alloc<double>(size_t(lm));
@@ -426,6 +431,19 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
     c.release(L.band, band_n);
     L.band = nb;
     L.sweep_tw = int(lm / ((long long)L.K * L.ext * L.Ob));
+  }
+  {
+    int front = 0, e2p = 0;
+    if (const long long lm = spmv_sweep3_band_doubles(d, p, L.ext, S, L.K, L.Ob != L.O, c.sweep3, &front, &e2p)) {
+      double* nb = c.alloc<double>(size_t(lm));
+      launch_sweep3_relayout(c.stream, p, L.ext, S, L.K, Sp, L.band, nb);
+      ck(cudaGetLastError(), "sweep3 relayout");
+      ck(cudaStreamSynchronize(c.stream), "sweep3 relayout");
+      c.release(L.band, band_n);
+      L.band = nb;
+      L.sweep3_front = front;
+      L.sweep3_e2p = e2p;
+    }
   }
   {
     long long nd = 0, nf = 0;
@@ -819,7 +837,7 @@ void build_ctx(pmg_ctx& c, const pmg_hierarchy_desc& D) {
   long long maxlat = 0;
   for (auto& L : c.lv) maxlat = std::max(maxlat, L.lat_n);
   c.partial_n = dot_blocks(maxlat);
-  for (auto& L : c.lv) c.partial_n = std::max(c.partial_n, spmv_partials(c.dim, c.degree, L.S, L.K, L.Ob != L.O, c.sweep));
+  for (auto& L : c.lv) c.partial_n = std::max(c.partial_n, spmv_partials(c.dim, c.degree, L.S, L.K, L.Ob != L.O, c.sweep, c.sweep3));
   c.partial = c.alloc<double>(size_t(c.partial_n));
   c.scal = c.alloc<double>(16);
   ck(cudaMemsetAsync(c.scal, 0, 16 * sizeof(double), c.stream), "memset");
@@ -881,7 +899,7 @@ void op_spmv(pmg_ctx& c, int l, const double* x, const double* f, double* y, dou
     throw PmgError(PMG_ERR_CONFIG, "half-band SpMV needs a 16-byte aligned x (TMA window)");
   TimedScope ts(c, 0, l, bytes);
   SpmvArgs a{c.dim, c.degree, L.ext, L.S, L.K, L.band, x, f, y, dot_partial, L.Ob != L.O, L.Sp, c.sweep,
-             L.sweep_scratch, L.sweep_flags, L.sweep_ticket};
+             L.sweep_scratch, L.sweep_flags, L.sweep_ticket, c.sweep3};
   launch_spmv(c.stream, a);
   c.launches++;
   c.spmv_launches++;
@@ -1226,7 +1244,7 @@ struct PcgParts {
   void front() {
     const DevLevel& F = c.lv[Lf];
     op_spmv(c, Lf, p, nullptr, Ap, c.partial);  // Ap and the partials of Ap.p
-    launch_sum_partials(c.stream, c.partial, spmv_partials(c.dim, c.degree, F.S, F.K, F.Ob != F.O, c.sweep), s + 1);
+    launch_sum_partials(c.stream, c.partial, spmv_partials(c.dim, c.degree, F.S, F.K, F.Ob != F.O, c.sweep, c.sweep3), s + 1);
     if (c.multi()) {  // pAp over all ranks, ascending rank order
       c.comm->allgather(c.stream, s + 1, c.rank_buf, 1);
       launch_sum_ranks(c.stream, c.rank_buf, c.size, 1, s + 1);
@@ -1588,9 +1606,11 @@ int pmg_band_download(pmg_ctx* ctx, int level, double* host, int64_t n) {
     ck(cudaMalloc(&tmp, per * sizeof(double)), "cudaMalloc band expand");
     try {
       for (int k = 0; k < L.K; ++k) {
-        const double* src = L.sweep_tw > 0 ? L.band + size_t(k) * L.ext * L.Ob * L.sweep_tw
-                                           : L.band + size_t(k) * L.Ob * L.Sp;
-        launch_band_expand(ctx->stream, ctx->dim, ctx->degree, L.ext, L.S, L.Ob, L.Sp, L.sweep_tw, src, tmp);
+        const double* src = L.sweep3_e2p > 0 ? L.band + size_t(k) * L.ext * L.Ob * L.sweep3_e2p
+                            : L.sweep_tw > 0  ? L.band + size_t(k) * L.ext * L.Ob * L.sweep_tw
+                                              : L.band + size_t(k) * L.Ob * L.Sp;
+        launch_band_expand(ctx->stream, ctx->dim, ctx->degree, L.ext, L.S, L.Ob, L.Sp, L.sweep_tw, L.sweep3_front,
+                           L.sweep3_e2p, src, tmp);
         ck(cudaGetLastError(), "band expand");
         ck(cudaMemcpyAsync(host + size_t(k) * per, tmp, per * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream),
            "band download");

@@ -149,6 +149,7 @@ struct SpmvArgs {
   double* sweep_scratch = nullptr;  // sweep: per segment boundary, the carry rows (spmv_sweep_scratch)
   unsigned* sweep_flags = nullptr;  // sweep: per segment boundary, carry published (zeroed; reset by the reader)
   unsigned long long* sweep_ticket = nullptr;  // sweep: segment ticket counter (zeroed, 8-byte aligned)
+  int sweep3 = 30;  // 3D half band: plane-sweep kernel on lattices of >= sweep3 rows per axis (0: off)
 };
 void launch_spmv(cudaStream_t s, const SpmvArgs& a);
 int spmv_blocks(long long rows);
@@ -161,7 +162,7 @@ bool spmv_tma_level(int dim, int degree, long long S);
 // allowed, else O
 int spmv_stored_offsets(int dim, int degree, long long S, bool allow_half);
 // number of dot partials one launch writes
-int spmv_partials(int dim, int degree, long long S, int K, bool half, int sweep);
+int spmv_partials(int dim, int degree, long long S, int K, bool half, int sweep, int sweep3);
 // scratch of a swept level: carry rows (doubles) and boundary flags (count)
 // 2D line-sweep levels keep the band line-major ([K][ext][Ob][tw], zero
 // padded): its size in doubles (0: the level is not swept), and the
@@ -171,13 +172,21 @@ void spmv_sweep_scratch(int dim, int degree, int ext, long long S, int K, bool h
                         long long* flags);
 void launch_sweep_relayout(cudaStream_t s, int degree, int ext, long long S, int K, long long Sp, const double* src,
                            double* dst);
-// One patch's device band (offset-major [Ob][Sp], or line-major [ext][Ob][tw]
-// when tw > 0) expanded to the reference's index-free full band [O][S]
+// One patch's device band (offset-major [Ob][Sp], line-major [ext][Ob][tw]
+// when tw > 0, plane-major [ext][Ob][e2p] when e2p > 0) expanded to the reference's index-free full band [O][S]
 // (offset o = sum_a (delta_a + p) (2p+1)^a, axis 0 fastest): stored offsets
 // are copied, the upper half of a symmetric half band is the mirrored lower
 // entry A(r, r+s) = A(r+s, r).  Pairs outside the lattice read 0.
 void launch_band_expand(cudaStream_t s, int dim, int degree, int ext, long long S, int Ob, long long Sp, int tw,
-                        const double* band_patch, double* full);
+                        int front, int e2p, const double* band_patch, double* full);
+// 3D plane-sweep levels keep the band plane-major ([K][ext][Ob][e2p], each
+// (plane, offset) row at [front, front + ext^2) between zero pads): its size
+// in doubles (0: the level is not swept) with front / e2p, and the conversion
+// from the offset-major band
+long long spmv_sweep3_band_doubles(int dim, int degree, int ext, long long S, int K, bool half, int sweep3,
+                                   int* front, int* e2p);
+void launch_sweep3_relayout(cudaStream_t s, int degree, int ext, long long S, int K, long long Sp, const double* src,
+                            double* dst);
 
 // ---------------------------------------------------------------- device PCG loop
 // State of a device-resident pcg_generic loop (multigrid.hpp:155-189): the

@@ -830,6 +830,323 @@ __global__ void __launch_bounds__(kSweepMaxExt + 32, 1) spmv_sweep2d_kernel(Spmv
   }
 }
 
+// ---------------------------------------------------------------- 3D plane sweep
+// 3D half band ([K][OB][Sp], offset-major).  A CTA owns the in-plane rows
+// [ta, tb) of one patch (a tile of the ext^2 rows of a lattice plane) and the
+// planes [Z0, Z1) of a segment, and sweeps them plane by plane.  For plane z
+// it streams, offset by offset, the band rows of its tile (one bulk copy per
+// offset: the rows (t, z) of the tile plus the |s_in| rows of halo the
+// mirrored use needs, s_in = d0 + d1 ext being the in-plane part of the
+// offset's shift s = s_in + d2 ext^2) and uses every value twice from shared
+// memory:
+//   lower     row (t, z):        += A(r, r + s) x(t + s_in, z + d2)
+//   mirrored  row (t, z + d2):   += A(r', r' + s) x(r'),  r' = (t - s_in, z)
+// (the mirrored term is the upper entry A(q, q - s) = A(q - s, q) of row q).
+// x of planes z-p..z+1 sits in a ring of p+3 plane slots (each the tile plus
+// p (1 + ext) rows of halo on both sides), filled one plane ahead.  Each
+// output row keeps p+1 plane accumulators in registers: plane z-p is
+// complete after plane z and is written then.  The mirrored terms a segment's
+// rows receive from the next segment's first p planes are computed by
+// streaming those planes as well (tail planes, only the offsets whose target
+// plane lies inside the segment), so CTAs never wait for each other.  Every
+// band value crosses HBM once; L2 serves the halo rows and the tail planes a
+// second time (about |s_in| / T and 1.7 / (Z1 - Z0) of the band).  Pairs
+// outside the tensor stencil hold exact zeros in the band (wrapped lines and
+// planes, Dirichlet, padding) and shared-memory rows outside the vectors hold
+// zeros, so no per-entry predicate is needed; offsets whose lower source
+// plane is below the lattice (z + d2 < 0) are all-zero and skipped.
+// Consumer thread i owns the rows ta + i + j NC, j < RPT (NC and RPT compile
+// time, so every shared-memory read is one LDS with an immediate offset);
+// rows past tb are computed on padding and not written.
+// Swept levels keep the band plane-major: [K][plane z][offset o][e2p], the
+// ext^2 rows of a (plane, offset) pair at [front, front + ext^2) between zero
+// pads that cover every halo and padding read (sweep3_relayout_kernel builds
+// it from the offset-major band once, at upload).  A CTA's stream of one
+// plane is then one contiguous block (ob e2p doubles): a few DRAM pages and
+// TLB entries per plane instead of one 2 MB offset row per stage.
+constexpr int kSweep3MaxStages = 24;
+constexpr int kSweep3Nc = 384;  // consumer threads (12 warps)
+constexpr int kSweep3Pw = 4;    // producer warps: warp w issues the stages st with st % kSweep3Pw == w
+constexpr int kSweep3MaxRpt = 4;
+
+struct Sweep3Cfg {
+  int tiles, T;     // in-plane tiles per plane, rows per tile
+  int zsegs, zlen;  // plane segments per patch, planes per segment
+  int rpt;          // rows per consumer thread (T <= rpt kSweep3Nc)
+  int ns, sd, xd;   // band ring stages, doubles per stage, doubles per x plane slot
+  int halo;         // p (1 + ext): the largest in-plane shift
+  int front, e2p;   // plane-major band: zero rows before a (plane, offset) row, row stride
+};
+
+template <int P>
+__device__ __forceinline__ int sweep3_shift(int o, int ext) {  // in-plane shift s_in of offset o
+  constexpr int W = 2 * P + 1;
+  const int q = o % (W * W);
+  return (q % W - P) + ext * (q / W - P);
+}
+
+template <int P, int RPT>
+struct Sweep3Consumer {
+  static constexpr int W = 2 * P + 1;
+  static constexpr int OB = (W * W * W + 1) / 2;
+  static constexpr int NX = P + 3;  // x plane slots
+  static constexpr int NA = P + 1;  // accumulator planes
+  static constexpr int NC = kSweep3Nc;
+  const SpmvArgs* a;
+  const double* ring;
+  const double* xs;
+  uint64_t *full, *empty, *xfull, *xempty;
+  long long E2, S;
+  int ext, k, ta, tb, Z0, Z1, Zend, zfirst, tid, st, ph, ns, sd, xd, halo;
+  double acc[NA][RPT];
+  double prod;
+
+  __device__ __forceinline__ const double* xp(int zz) const {  // xp(zz)[i] = x(i, zz) of patch k
+    const int sl = (zz - zfirst) % NX;
+    const long long g0 = (long long)k * S + (long long)zz * E2 + ta - halo;
+    return xs + sl * xd + int(g0 & 1) + (halo - ta);
+  }
+  __device__ __forceinline__ void wait_x(int zz) {
+    const int u = zz - zfirst;
+    mbar_wait(&xfull[u % NX], (u / NX) & 1);
+  }
+  __device__ __forceinline__ void finish(int zo, double (&accz)[RPT]) {  // plane zo complete
+    const double* xz = xp(zo);
+    const long long base = (long long)k * S + (long long)zo * E2;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int t = ta + tid + j * NC;
+      if (t < tb) {
+        const double y = a->f ? a->f[base + t] - accz[j] : accz[j];
+        a->y[base + t] = y;
+        if (a->dot_partial) prod = fma(y, xz[t], prod);
+      }
+      accz[j] = 0.0;
+    }
+  }
+  // the offsets [o_beg, o_end) of one d2 group (GI = d2 + p) at plane z
+  template <int ZS, int GI, bool LOWER, bool MIRROR>
+  __device__ __forceinline__ void offsets(int o_beg, int o_end, int base_par, const double* xl, const double* xz) {
+    int d0 = (o_beg % W) - P;
+    int s_in = sweep3_shift<P>(o_beg, ext);
+    const double* xlt = xl + ta + tid;  // xlt[j NC] = x(ta + tid + j NC, z + d2)
+    const double* xzt = xz + ta + tid;
+    for (int o = o_beg; o < o_end; ++o) {
+      const int sc = st;
+      mbar_wait(&full[sc], ph);
+      if (++st == ns) {
+        st = 0;
+        ph ^= 1;
+      }
+      const int lo_rel = min(0, -s_in);
+      const int par = (base_par ^ lo_rel) & 1;  // parity of the stage's first in-plane index
+      const double* bp = ring + sc * sd + par - lo_rel + tid;  // bp[j NC] = band row (ta + tid + j NC, z)
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        if (LOWER) acc[ZS][j] = fma(bp[j * NC], xlt[j * NC + s_in], acc[ZS][j]);
+        // target slot (ZS + d2) mod (p+1) = (ZS + GI + 1) mod (p+1)
+        if (MIRROR)
+          acc[(ZS + GI + 1) % NA][j] = fma(bp[j * NC - s_in], xzt[j * NC - s_in], acc[(ZS + GI + 1) % NA][j]);
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[sc]);
+      if (++d0 > P) {
+        d0 = -P;
+        s_in += ext - 2 * P;
+      } else {
+        s_in += 1;
+      }
+    }
+  }
+  template <int ZS, int GI>
+  __device__ __forceinline__ void group(int z, int base_par, const double* xz) {
+    const int zt = z + GI - P;  // mirrored target plane / lower source plane
+    const bool in_seg = z < Z1;
+    if ((!in_seg && zt >= Z1) || zt < 0) return;  // skipped by the producer as well
+    const bool mirror = zt >= Z0 && zt < Z1;
+    const double* xl = in_seg ? xp(zt) : xz;
+    const int o_beg = GI * W * W;
+    const int o_end = GI < P ? (GI + 1) * W * W : OB - 1;  // the centre (diagonal) separately
+    if (in_seg && mirror)
+      offsets<ZS, GI, true, true>(o_beg, o_end, base_par, xl, xz);
+    else if (in_seg)
+      offsets<ZS, GI, true, false>(o_beg, o_end, base_par, xl, xz);
+    else
+      offsets<ZS, GI, false, true>(o_beg, o_end, base_par, xl, xz);
+    if (GI == P && in_seg) offsets<ZS, GI, true, false>(OB - 1, OB, base_par, xl, xz);
+  }
+  // one plane step; ZS = (z - Z0) mod (p+1) is the accumulator slot of plane z
+  template <int ZS>
+  __device__ __forceinline__ void plane(int z) {
+    wait_x(z);
+    const double* xz = xp(z);
+    const int base_par = ta & 1;
+    group<ZS, 0>(z, base_par, xz);
+    if (P >= 1) group<ZS, 1 % (P + 1)>(z, base_par, xz);
+    if (P >= 2) group<ZS, 2 % (P + 1)>(z, base_par, xz);
+    if (P >= 3) group<ZS, 3 % (P + 1)>(z, base_par, xz);
+    const int zo = z - P;  // complete now
+    if (zo >= Z0 && zo < Z1) finish(zo, acc[(ZS + 1) % NA]);
+    if (zo >= zfirst) {  // x plane zo is no longer read
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&xempty[(zo - zfirst) % NX]);
+    }
+  }
+};
+
+template <int P, int RPT>
+__global__ void __launch_bounds__(kSweep3Nc + 32 * kSweep3Pw, 1) spmv_sweep3d_kernel(SpmvArgs a, Sweep3Cfg g) {
+  PMG_PDL_ENTRY();
+  using C = Sweep3Consumer<P, RPT>;
+  constexpr int OB = C::OB;
+  constexpr int NX = C::NX;
+  constexpr int NA = C::NA;
+  constexpr int NC = kSweep3Nc;
+  extern __shared__ __align__(128) double smem[];  // [ns][sd] band ring, [NX][xd] x planes
+  __shared__ __align__(8) uint64_t full[kSweep3MaxStages], empty[kSweep3MaxStages], xfull[NX], xempty[NX];
+  __shared__ double red[NC / 32];
+
+  const int ext = a.ext;
+  const long long E2 = (long long)ext * ext;
+  const long long S = a.S;
+  const int tid = threadIdx.x;
+  const int tile = blockIdx.x % g.tiles;
+  const int zs = (blockIdx.x / g.tiles) % g.zsegs;
+  const int k = blockIdx.x / (g.tiles * g.zsegs);
+  const int ta = tile * g.T;
+  const int tb = min(int(E2), ta + g.T);
+  const int Z0 = zs * g.zlen;
+  const int Z1 = min(ext, Z0 + g.zlen);
+  const int Zend = min(ext, Z1 + P);
+  const int zfirst = max(0, Z0 - P);
+  double* xs = smem + (size_t)g.ns * g.sd;
+  if (tid == 0) {
+    for (int s = 0; s < g.ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NC / 32);
+    }
+    for (int s = 0; s < NX; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], NC / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (tid >= NC) {  // producers: one bulk copy per (plane, offset); x planes from warp 0
+    const int pw = (tid - NC) >> 5;
+    if (((tid - NC) & 31) == 0) {
+      const long long total = S * a.K;
+      const int H = g.halo;
+      const int Tpad = RPT * NC;  // rows computed per tile (padding past tb included)
+      auto load_x = [&](int zz) {
+        const int u = zz - zfirst;
+        const int sl = u % NX;
+        if (u >= NX) mbar_wait(&xempty[sl], ((u / NX) - 1) & 1);
+        double* dst = xs + (size_t)sl * g.xd;
+        long long g0 = (long long)k * S + (long long)zz * E2 + ta - H;
+        g0 -= g0 & 1;
+        const long long n = g.xd;
+        const long long lo = g0 < 0 ? 0 : g0;
+        const long long hi = g0 + n > total ? total : g0 + n;
+        const long long th = lo + ((hi - lo) & ~1LL);  // bulk part [lo, th), 16-byte sized
+        for (long long e = g0; e < lo; ++e) dst[e - g0] = 0.0;  // before the vector
+        for (long long e = th; e < g0 + n; ++e) dst[e - g0] = e < total ? a.x[e] : 0.0;  // odd end / past it
+        mbar_expect_tx(&xfull[sl], unsigned((th - lo) * sizeof(double)));
+        if (th > lo) tma_load_1d(dst + (lo - g0), a.x + lo, unsigned((th - lo) * sizeof(double)), &xfull[sl]);
+      };
+      if (pw == 0)
+        for (int zz = zfirst; zz <= Z0; ++zz) load_x(zz);
+      int s = 0, round = 0;  // ring slot and how many times the ring has been filled
+      int seq = 0;           // stage sequence number
+      for (int z = Z0; z < Zend; ++z) {
+        if (pw == 0 && z + 1 < Zend) load_x(z + 1);
+        for (int o = 0; o < OB; ++o) {
+          constexpr int W = 2 * P + 1;
+          const int zt = z + o / (W * W) - P;
+          if ((z >= Z1 && zt >= Z1) || zt < 0) continue;  // no target in the segment / all-zero offset
+          const int mine = (seq++ % kSweep3Pw) == pw;
+          if (!mine) {
+            if (++s == g.ns) {
+              s = 0;
+              ++round;
+            }
+            continue;
+          }
+          const int s_in = sweep3_shift<P>(o, ext);
+          if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+          const int lo_in = ta + min(0, -s_in);
+          const int hi_in = ta + Tpad + max(0, -s_in);
+          const int r0 = lo_in - (lo_in & 1);  // in-plane index of the stage's first element (even)
+          const int n = (hi_in - r0 + 1) & ~1;
+          const double* src = a.band + (((size_t)k * ext + z) * OB + o) * g.e2p + g.front + r0;
+          mbar_expect_tx(&full[s], unsigned(n * sizeof(double)));
+          tma_load_1d(smem + (size_t)s * g.sd, src, unsigned(n * sizeof(double)), &full[s]);
+          if (++s == g.ns) {
+            s = 0;
+            ++round;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  C c;
+  c.a = &a;
+  c.ring = smem;
+  c.xs = xs;
+  c.full = full;
+  c.empty = empty;
+  c.xfull = xfull;
+  c.xempty = xempty;
+  c.E2 = E2;
+  c.S = S;
+  c.ext = ext;
+  c.k = k;
+  c.ta = ta;
+  c.tb = tb;
+  c.Z0 = Z0;
+  c.Z1 = Z1;
+  c.Zend = Zend;
+  c.zfirst = zfirst;
+  c.tid = tid;
+  c.st = 0;
+  c.ph = 0;
+  c.ns = g.ns;
+  c.sd = g.sd;
+  c.xd = g.xd;
+  c.halo = g.halo;
+  c.prod = 0.0;
+#pragma unroll
+  for (int q = 0; q < NA; ++q)
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) c.acc[q][j] = 0.0;
+  for (int zz = zfirst; zz < Z0; ++zz) c.wait_x(zz);
+  for (int zb = Z0; zb < Zend; zb += NA) {
+    c.template plane<0>(zb);
+    if (zb + 1 < Zend) c.template plane<1 % NA>(zb + 1);
+    if (P >= 2 && zb + 2 < Zend) c.template plane<2 % NA>(zb + 2);
+    if (P >= 3 && zb + 3 < Zend) c.template plane<3 % NA>(zb + 3);
+  }
+  // planes not written yet: the last segment of a patch has no tail planes
+#pragma unroll
+  for (int q = 0; q < NA; ++q)
+    for (int zo = max(Z0, Zend - P); zo < Z1; ++zo)
+      if ((zo - Z0) % NA == q) c.finish(zo, c.acc[q]);
+  if (a.dot_partial) {
+    double prod = c.prod;
+    for (int o = 16; o > 0; o >>= 1) prod += __shfl_down_sync(0xffffffffu, prod, o);
+    if ((tid & 31) == 0) red[tid >> 5] = prod;
+    asm volatile("bar.sync 1, %0;\n" ::"n"(NC) : "memory");
+    if (tid == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < NC / 32; ++w) sum += red[w];
+      a.dot_partial[blockIdx.x] = sum;
+    }
+  }
+}
+
 template <int D, int P>
 void launch_tma(cudaStream_t s, const SpmvArgs& a) {
   constexpr int W = 2 * P + 1;
@@ -946,7 +1263,7 @@ int spmv_blocks(long long rows) { return int((rows + kThreads - 1) / kThreads); 
 
 namespace {
 __global__ void band_expand_kernel(const double* __restrict__ band, double* __restrict__ full, int dim, int p,
-                                   int ext, long long S, int O, int Ob, long long Sp, int tw) {
+                                   int ext, long long S, int O, int Ob, long long Sp, int tw, int front, int e2p) {
   const int W = 2 * p + 1;
   const int padl = (p + 1) & ~1;
   const long long n = (long long)O * S;
@@ -968,7 +1285,10 @@ __global__ void band_expand_kernel(const double* __restrict__ band, double* __re
     }
     double v = 0.0;
     if (row >= 0 && row < S) {
-      if (tw > 0) {
+      if (e2p > 0) {  // plane-major 3D sweep layout
+        const long long E2 = (long long)ext * ext;
+        v = band[((row / E2) * Ob + ob) * e2p + front + row % E2];
+      } else if (tw > 0) {
         const long long L = row / ext;
         const int i = int(row % ext);
         v = band[(L * Ob + ob) * tw + padl + i];
@@ -982,10 +1302,10 @@ __global__ void band_expand_kernel(const double* __restrict__ band, double* __re
 }  // namespace
 
 void launch_band_expand(cudaStream_t s, int dim, int degree, int ext, long long S, int Ob, long long Sp, int tw,
-                        const double* band_patch, double* full) {
+                        int front, int e2p, const double* band_patch, double* full) {
   const int W = 2 * degree + 1;
   const int O = dim == 2 ? W * W : W * W * W;
-  band_expand_kernel<<<148 * 8, 256, 0, s>>>(band_patch, full, dim, degree, ext, S, O, Ob, Sp, tw);
+  band_expand_kernel<<<148 * 8, 256, 0, s>>>(band_patch, full, dim, degree, ext, S, O, Ob, Sp, tw, front, e2p);
 }
 
 long long spmv_sweep_band_doubles(int dim, int degree, int ext, long long S, int K, bool half, int sweep) {
@@ -1019,17 +1339,135 @@ void launch_sweep_relayout(cudaStream_t s, int degree, int ext, long long S, int
   }
 }
 
+// 3D plane-sweep configuration of one level: in-plane tiles and plane
+// segments so that the CTAs fill the GPU in one wave (one CTA per SM: the
+// consumers hold ~90 registers and a deep ring keeps enough band bytes in
+// flight), with the least re-read band (halo rows |s_in| / T, tail planes
+// ~1.7 / zlen); the ring depth from the shared-memory budget.  sweep3 = the
+// shortest lattice axis swept (PMG_SWEEP3D at context creation; 0 disables).
+static bool sweep3_cfg(int dim, int degree, int ext, long long S, int K, bool half, int sweep3, Sweep3Cfg* out,
+                       size_t* smem_out) {
+  if (sweep3 <= 0 || dim != 3 || !half || (degree != 2 && degree != 3) || ext < sweep3 || ext < 4 * degree)
+    return false;
+  (void)S;
+  const long long E2 = (long long)ext * ext;
+  const int H = degree * (1 + ext);
+  const int sms = sm_count();
+  const size_t budget = 227 * 1024 - 2048;
+  double best = 1e30;
+  bool found = false;
+  for (int tiles = 1; tiles <= 32; ++tiles) {
+    const int T = int((E2 + tiles - 1) / tiles);
+    if (T < 96) break;
+    const int rpt = (T + kSweep3Nc - 1) / kSweep3Nc;
+    if (rpt > kSweep3MaxRpt) continue;
+    const int tpad = rpt * kSweep3Nc;
+    const int sd = (tpad + H + 5) & ~1;
+    const int xd = (tpad + 2 * H + 5) & ~1;
+    const size_t xbytes = size_t(degree + 3) * xd * sizeof(double);
+    if (xbytes + 4 * size_t(sd) * sizeof(double) > budget) continue;
+    static const int ns_cap = env_int("PMG_SWEEP3_NS", kSweep3MaxStages);  // ring depth cap (experiments)
+    const int ns = int(std::min<size_t>(std::min(kSweep3MaxStages, ns_cap),
+                                        (budget - xbytes) / (size_t(sd) * sizeof(double))));
+    for (int zsegs = 1; zsegs <= 16; ++zsegs) {
+      const int zlen = (ext + zsegs - 1) / zsegs;
+      if (zlen < 2 * degree) break;
+      const int nz = (ext + zlen - 1) / zlen;
+      const long long ctas = (long long)K * tiles * nz;
+      if (ctas > sms) break;  // one wave: CTAs run start to end
+      const double fill = std::min(1.0, double(ctas) / (0.9 * sms));
+      const double cost = (double(tpad) / T + 0.5 * H / T) * (1.0 + (nz > 1 ? 1.7 / zlen : 0.0)) / fill;
+      if (cost < best) {
+        best = cost;
+        found = true;
+        out->tiles = tiles;
+        out->T = T;
+        out->zsegs = nz;
+        out->zlen = zlen;
+        out->rpt = rpt;
+        out->ns = ns;
+        out->sd = sd;
+        out->xd = xd;
+        out->halo = H;
+        // zero pads: reads reach in-plane indices [-H - 1, ta + tpad + H], ta + tpad <= E2 + tiles + NC
+        out->front = (H + 3) & ~1;
+        out->e2p = (out->front + int(E2) + H + kSweep3Nc + tiles + 8) & ~1;
+        *smem_out = size_t(ns) * sd * sizeof(double) + xbytes;
+      }
+    }
+  }
+  return found;
+}
+
+template <int P>
+void launch_sweep3(cudaStream_t s, const SpmvArgs& a, const Sweep3Cfg& g, size_t smem) {
+  const dim3 grid(unsigned(a.K * g.tiles * g.zsegs)), block(kSweep3Nc + 32 * kSweep3Pw);
+#define PMG_SWEEP3_CASE(R)                                                      \
+  if (g.rpt == R) {                                                             \
+    ensure_smem((const void*)spmv_sweep3d_kernel<P, R>, smem);                  \
+    launch_k(spmv_sweep3d_kernel<P, R>, grid, block, smem, s, a, g);            \
+    return;                                                                     \
+  }
+  PMG_SWEEP3_CASE(1) PMG_SWEEP3_CASE(2) PMG_SWEEP3_CASE(3) PMG_SWEEP3_CASE(4)
+#undef PMG_SWEEP3_CASE
+}
+
+namespace {
+// offset-major [K][OB][Sp] -> plane-major [K][ext][OB][e2p] with zero pads
+__global__ void sweep3_relayout_kernel(const double* __restrict__ src, double* __restrict__ dst, int ext, int K,
+                                       int OB, long long Sp, int front, int e2p) {
+  const long long E2 = (long long)ext * ext;
+  const long long n = (long long)K * ext * OB * e2p;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int c = int(e % e2p);
+    const long long t = e / e2p;
+    const int o = int(t % OB);
+    const long long kz = t / OB;
+    const int z = int(kz % ext);
+    const long long k = kz / ext;
+    const long long i = c - front;
+    dst[e] = (i >= 0 && i < E2) ? src[((size_t)k * OB + o) * Sp + (size_t)z * E2 + i] : 0.0;
+  }
+}
+}  // namespace
+
+long long spmv_sweep3_band_doubles(int dim, int degree, int ext, long long S, int K, bool half, int sweep3,
+                                   int* front, int* e2p) {
+  Sweep3Cfg g;
+  size_t smem;
+  if (!sweep3_cfg(dim, degree, ext, S, K, half, sweep3, &g, &smem)) return 0;
+  const int W = 2 * degree + 1;
+  *front = g.front;
+  *e2p = g.e2p;
+  return (long long)K * ext * ((W * W * W + 1) / 2) * g.e2p;
+}
+
+void launch_sweep3_relayout(cudaStream_t s, int degree, int ext, long long S, int K, long long Sp, const double* src,
+                            double* dst) {
+  Sweep3Cfg g;
+  size_t smem;
+  if (!sweep3_cfg(3, degree, ext, S, K, true, 1, &g, &smem)) return;
+  const int W = 2 * degree + 1;
+  sweep3_relayout_kernel<<<148 * 8, 256, 0, s>>>(src, dst, ext, K, (W * W * W + 1) / 2, Sp, g.front, g.e2p);
+}
+
 static int ext_of(int dim, long long S) {
-  if (dim != 2) return 0;
   long long e = 1;
-  while (e * e < S) ++e;
+  if (dim == 2) {
+    while (e * e < S) ++e;
+  } else {
+    while (e * e * e < S) ++e;
+  }
   return int(e);
 }
 
-int spmv_partials(int dim, int degree, long long S, int K, bool half, int sweep) {
+int spmv_partials(int dim, int degree, long long S, int K, bool half, int sweep, int sweep3) {
   SweepCfg g;
   size_t smem;
-  if (sweep_cfg(dim, degree, ext_of(dim, S), S, K, half, sweep, &g, &smem)) return g.segs * K;
+  if (dim == 2 && sweep_cfg(dim, degree, ext_of(dim, S), S, K, half, sweep, &g, &smem)) return g.segs * K;
+  Sweep3Cfg g3;
+  if (dim == 3 && sweep3_cfg(dim, degree, ext_of(dim, S), S, K, half, sweep3, &g3, &smem))
+    return K * g3.tiles * g3.zsegs;
   if (spmv_tma_level(dim, degree, S)) return int((S + kRowsTma - 1) / kRowsTma * K);
   return spmv_blocks(S * K);
 }
@@ -1043,6 +1481,13 @@ void launch_spmv(cudaStream_t s, const SpmvArgs& a) {
       case 2: launch_sweep<2>(s, a, g, smem); return;
       case 3: launch_sweep<3>(s, a, g, smem); return;
       case 4: launch_sweep<4>(s, a, g, smem); return;
+    }
+  }
+  Sweep3Cfg g3;
+  if (sweep3_cfg(a.dim, a.degree, a.ext, a.S, a.K, a.half != 0, a.sweep3, &g3, &smem)) {
+    switch (a.degree) {
+      case 2: launch_sweep3<2>(s, a, g3, smem); return;
+      case 3: launch_sweep3<3>(s, a, g3, smem); return;
     }
   }
   if (spmv_tma_level(a.dim, a.degree, a.S)) {

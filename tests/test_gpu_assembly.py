@@ -59,7 +59,8 @@ def test_pcg_on_device_assembled_hierarchy(dom, p, lv, n0):
 
 @pytest.mark.parametrize("dom,p,lv,n0,env", [
     ("c2", 4, 5, 2, {}), ("c2", 4, 5, 2, {"PMG_SWEEP_MIN_EXT": "1"}),  # offset-major and line-major levels
-    ("c2", 4, 4, 2, {"PMG_FULL_BAND": "1"}), ("c4", 3, 3, 2, {}), ("c3", 8, 3, 2, {}), ("fichera", 2, 3, 1, {})])
+    ("c2", 4, 4, 2, {"PMG_FULL_BAND": "1"}), ("c4", 3, 3, 2, {}), ("c3", 8, 3, 2, {}), ("fichera", 2, 3, 1, {}),
+    ("c4", 3, 3, 2, {"PMG_SWEEP3D": "12"})])  # plane-major band of the 3D plane sweep
 def test_band_download_feeds_the_oracle(dom, p, lv, n0, env, monkeypatch):
     """pmg_band_download: a device-assembled hierarchy hands its bands to the
     host (Hierarchy.adopt_device_bands); the oracle on those bands applies the

@@ -46,7 +46,7 @@ def test_reference_templates_drive_the_gpu_backend(args):
     assert out.returncode == 0, out.stderr
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["template_iterations"] == res["fused_iterations"]
-    assert res["max_rel_diff"] < 1e-10 and res["history_max_rel_diff"] < 1e-8
+    assert res["max_rel_diff"] < 1e-10 and res["history_head_max_rel_diff"] < 1e-10
     assert res["domain_error"] and res["divergence_error"]
     dom, p, lv, n0 = args
     h = Hierarchy(dom, p, lv, n0=n0)

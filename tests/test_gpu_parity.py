@@ -299,3 +299,42 @@ def test_device_loop_matches_host_loop(dom, p, lv, n0, monkeypatch):
     # and the solve still works after the error paths
     u3, rep3 = b.pcg_solve(f)
     assert np.array_equal(u3, u1)
+
+
+@pytest.mark.parametrize("dom,p,lv,n0,min_ext", [
+    # PMG_SWEEP3D=<n> sweeps every 3D level whose lattice has >= n rows per axis
+    ("c4", 3, 2, 2, "12"), ("c4", 3, 3, 2, "12"), ("c5", 3, 3, 2, "12"), ("c4", 3, 4, 2, "12"),
+    ("fichera", 2, 4, 1, "8"), ("c4", 2, 4, 2, "8"), ("c5", 2, 3, 2, "8"),
+    ("c4", 3, 4, 2, "30")])  # the default threshold: only lattices of >= 30 rows per axis
+def test_plane_sweep_matches_tma_half(dom, p, lv, n0, min_ext, monkeypatch):
+    """3D plane-sweep SpMV (spmv_sweep3d_kernel: in-plane tiles x plane
+    segments, every half-band value used as lower and mirrored upper entry
+    from shared memory) against the 256-row TMA half-band kernel
+    (PMG_SWEEP3D=0) and the oracle on every level, including one- and
+    several-segment sweeps, partial last tiles, p = 2 and 3, the residual
+    form and the dot partials of Ap.p inside PCG."""
+    h = Hierarchy(dom, p, lv, n0=n0)
+    out = {}
+    for mode in (min_ext, "0"):
+        monkeypatch.setenv("PMG_SWEEP3D", mode)
+        b = GpuBackend(h)
+        res = []
+        for level in range(h.num_levels):
+            u = rand(h.num_dofs(level), 31 + level)
+            f = rand(h.num_dofs(level), 71 + level)
+            res.append((b.gather_global(level, b.apply_op(level, b.to_accumulated(level, u))),
+                        b.gather_global(level, b.residual(level, b.to_distributed_owner(level, f),
+                                                          b.to_accumulated(level, u)))))
+        u_sol, rep = b.pcg_solve(h.rhs())
+        out[mode] = (res, u_sol, rep.iterations)
+        del b
+    ref = oracle.Oracle(h)
+    for level in range(h.num_levels):
+        u = rand(h.num_dofs(level), 31 + level)
+        f = rand(h.num_dofs(level), 71 + level)
+        for j in range(2):
+            assert rel(out[min_ext][0][level][j], out["0"][0][level][j]) < 1e-14, (level, j)
+        assert rel(out[min_ext][0][level][0], ref.apply_op(level, u)) < 1e-13
+        assert rel(out[min_ext][0][level][1], ref.residual(level, f, u)) < 1e-13
+    assert out[min_ext][2] == out["0"][2]
+    assert rel(out[min_ext][1], out["0"][1]) < 1e-10
