@@ -84,6 +84,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target length of the CPU sample")
+    ap.add_argument("--operator", default="band", choices=["band", "kronecker"],
+                    help="patch operator on the device: the assembled band, or matrix-free as a Kronecker sum "
+                         "(axis-aligned affine configs: c1, c3*)")
     ap.add_argument("--assembly", default=None, choices=["host", "device"],
                     help="stiffness assembly of levels >= 1 (default: device for 3D, host for 2D)")
     return ap.parse_args()
@@ -186,7 +189,8 @@ def build_hierarchy(args, world=1, threads=None, assembly=None):
     dom, p, n0, lv = domain_of(args, world)
     if args.levels is not None:
         lv = args.levels
-    return Hierarchy(dom, p, lv, n0=n0, seed=args.seed, threads=threads, assembly=assembly or "host")
+    return Hierarchy(dom, p, lv, n0=n0, seed=args.seed, threads=threads, assembly=assembly or "host",
+                     operator=args.operator)
 
 
 def default_assembly(args):
@@ -513,16 +517,21 @@ def main():
              5: "coarse_solve"}
     breakdown = {names[c]: {"ms_per_step": cls_ms[c] / steps, "share_of_step": cls_ms[c] / steps / ms_step}
                  for c in range(6)}
+    if args.operator == "kronecker":
+        kernel_desc = ("kron2d_kernel / kron3d_axis*_kernel (matrix-free Kronecker-sum operator, PMG_BAND_KRONECKER), "
+                       "finest level; bytes = 8 B per lattice row for x, y (and f) + 4 B for the Dirichlet map")
+    else:
+        kernel_desc = (("spmv_sweep2d_kernel (2D line sweep over the line-major symmetric half band: each band "
+                        "value read once from HBM and used as lower and mirrored upper entry from shared memory)"
+                        if h.dim == 2 else
+                        "spmv_sweep3d_kernel (3D plane sweep over the plane-major symmetric half band: each band "
+                        "value read once from HBM and used as lower and mirrored upper entry from shared memory)")
+                       + ", finest level; bytes = half band 8 (S + D) / 2 + 8 B per lattice row for x, y (and f), "
+                         "SURVEY.md 8(d), DESIGN.md 3")
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
         "frac": (achieved / hbm) if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
-        "kernel": (("spmv_sweep2d_kernel (2D line sweep over the line-major symmetric half band: each band "
-                    "value read once from HBM and used as lower and mirrored upper entry from shared memory)"
-                    if h.dim == 2 else
-                    "spmv_tma_half_kernel (index-free symmetric half-band SpMV / residual, TMA bulk-copy stream; "
-                    "mirrored half re-read from L2)")
-                   + ", finest level; bytes = half band 8 (S + D) / 2 + 8 B per lattice row for x, y (and f), "
-                     "SURVEY.md 8(d), DESIGN.md 3"),
+        "kernel": kernel_desc,
         "launches": sp_n, "avg_ms": sp_ms / max(sp_n, 1), "bytes_per_launch": sp_bytes / max(sp_n, 1),
         "peak_source": hbm_src,
         "timing": "CUDA events around every finest-level launch in an instrumented replay of the same K steps "
@@ -554,7 +563,7 @@ def main():
         "data": "synthetic (seeded generator of the BASELINE config; see DESIGN.md)",
         "config": workload_config(args, h, world, {
             "pcg_iterations": iters, "final_rel_residual": rel_res, "tol_margin": 1e-8 / rel_res,
-            "assembly": assembly,
+            "assembly": assembly, "operator": args.operator,
             "setup_s": {"host_setup": t_setup, "host_assembly": h.assemble_seconds(),
                         "device_assembly": b.assembly_seconds()},
             "solve_ms": ms_step}),

@@ -36,8 +36,11 @@ enum {
 int pmgh_build(const char* domain, int split, int degree, int n0, int levels, const pmg_cycle_params* params,
                int rhs_kind, uint64_t seed, int threads, pmgh_hierarchy** out);
 /* flags: PMGH_DEVICE_ASSEMBLY leaves the stiffness of levels >= 1 unassembled
- * (PMG_BAND_ASSEMBLE): the CUDA context assembles it from the patch geometry. */
-enum { PMGH_DEVICE_ASSEMBLY = 1 };
+ * (PMG_BAND_ASSEMBLE): the CUDA context assembles it from the patch geometry.
+ * PMGH_KRONECKER describes levels >= 1 as PMG_BAND_KRONECKER: the CUDA context
+ * applies the operator matrix-free (axis-aligned affine patch maps only); the
+ * host band, when assembled, stays in the descriptor for host-side checkers. */
+enum { PMGH_DEVICE_ASSEMBLY = 1, PMGH_KRONECKER = 2 };
 int pmgh_build_ex(const char* domain, int split, int degree, int n0, int levels, const pmg_cycle_params* params,
                   int rhs_kind, uint64_t seed, int threads, int flags, pmgh_hierarchy** out);
 void pmgh_free(pmgh_hierarchy* h);

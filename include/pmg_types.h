@@ -46,8 +46,16 @@ enum { PMG_PIECE_INTERIOR = 0, PMG_PIECE_FACE = 1, PMG_PIECE_EDGE = 2, PMG_PIECE
  *   PMG_BAND_CSR:      the reference PatchOperator triple per patch.
  *   PMG_BAND_ASSEMBLE: no values; the context assembles the band on the device
  *                      from pmg_hierarchy_desc.geometry (assemble_patch_stiffness,
- *                      assembly.cpp:127-248, with Gauss-Legendre p+1 points). */
-enum { PMG_BAND_TENSOR = 0, PMG_BAND_CSR = 1, PMG_BAND_ASSEMBLE = 2 };
+ *                      assembly.cpp:127-248, with Gauss-Legendre p+1 points).
+ *   PMG_BAND_KRONECKER: no values read; the context applies the patch operator
+ *                      matrix-free as the Kronecker sum of the univariate mass
+ *                      and stiffness matrices (the identity the reference tests in
+ *                      test_assembly.cpp:112-146).  Every patch map in
+ *                      pmg_hierarchy_desc.geometry must be axis-aligned affine,
+ *                      x_a = c_a + h_a xi_a; pmg_ctx_create returns PMG_ERR_CONFIG
+ *                      otherwise.  Results agree with the assembled band to
+ *                      rounding (about 1e-15 relative), not bitwise. */
+enum { PMG_BAND_TENSOR = 0, PMG_BAND_CSR = 1, PMG_BAND_ASSEMBLE = 2, PMG_BAND_KRONECKER = 3 };
 
 /* Geometry of one patch (GeometryMap, geometry.hpp): a tensor B-spline map
  * whose axis a uses the uniform open-knot space of degree[a] with elements[a]
@@ -115,7 +123,7 @@ typedef struct {
   int coarse_n;
   const double* coarse_A; /* dense, column-major */
   const double* coarse_L; /* lower Cholesky factor of coarse_A, column-major */
-  /* per patch; required when a level uses PMG_BAND_ASSEMBLE, else may be NULL */
+  /* per patch; required when a level uses PMG_BAND_ASSEMBLE or PMG_BAND_KRONECKER, else may be NULL */
   const pmg_patch_geometry* geometry;
 } pmg_hierarchy_desc;
 

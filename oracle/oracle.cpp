@@ -71,7 +71,9 @@ void build_view(const pmg_hierarchy_desc* D, Hier& H) {
   H.lv.resize(D->num_levels);
   for (int l = 0; l < D->num_levels; ++l) {
     const pmg_level_desc& ld = D->levels[l];
-    if (ld.band_format != PMG_BAND_TENSOR || !ld.band)
+    // a PMG_BAND_KRONECKER level still carries the host-assembled band: the
+    // checker applies the assembled operator, as the reference does
+    if ((ld.band_format != PMG_BAND_TENSOR && ld.band_format != PMG_BAND_KRONECKER) || !ld.band)
       throw ConfigError("oracle: needs host-assembled tensor bands (use a host-assembled hierarchy)");
     Level& L = H.lv[l];
     L.desc = &ld;

@@ -41,8 +41,8 @@ class PmgPatchGeometry(C.Structure):
     _fields_ = [("degree", C.c_int * 3), ("elements", C.c_int * 3), ("ctrl", C.POINTER(C.c_double))]
 
 
-PMG_BAND_TENSOR, PMG_BAND_CSR, PMG_BAND_ASSEMBLE = 0, 1, 2
-PMGH_DEVICE_ASSEMBLY = 1
+PMG_BAND_TENSOR, PMG_BAND_CSR, PMG_BAND_ASSEMBLE, PMG_BAND_KRONECKER = 0, 1, 2, 3
+PMGH_DEVICE_ASSEMBLY, PMGH_KRONECKER = 1, 2
 
 
 class PmgHierarchyDesc(C.Structure):

@@ -27,6 +27,7 @@
 
 #include "../../../include/pmg_cuda.h"
 #include "../common/rank_plan.hpp"
+#include "../host/numerics.hpp"
 #include "comm.cuh"
 #include "internal.cuh"
 
@@ -50,6 +51,10 @@ struct DevLevel {
   int sweep3_front = 0, sweep3_e2p = 0;  // e2p > 0: plane-major [K][ext][Ob][e2p] (3D plane-sweep level)
   long long S = 0, Sp = 0, lat_n = 0, N = 0;
   double* band = nullptr;
+  // PMG_BAND_KRONECKER level (kernels_kron.cu): no band; univariate mass and
+  // stiffness as full bands [ext][2p+1], per-patch geometry factors [K][3]
+  bool kron = false;
+  double *kron_M = nullptr, *kron_K = nullptr, *kron_g = nullptr, *kron_scratch = nullptr;
   double* sweep_scratch = nullptr;  // line sweep: segment-boundary rows
   unsigned* sweep_flags = nullptr;
   unsigned long long* sweep_ticket = nullptr;
@@ -72,7 +77,7 @@ struct DevLevel {
   int n_int = 0;
   int4* int_items[6] = {};
   int n_int_items[6] = {};
-  int int_ntc[6] = {};
+  int int_ntc[6] = {};  // kernel configuration per pass (fd_pick_cfg)
   std::vector<std::array<int, 3>> int_dims;  // host copy for flop counts
   bool int_small = false, face_small = false;  // whole solve per CTA in shared memory
   long long int_max_total = 0, face_max_total = 0;
@@ -339,6 +344,11 @@ std::vector<double> spd_inverse(int n, const double* L) {
   return inv;
 }
 
+int level_spmv_partials(const pmg_ctx& c, const DevLevel& L);
+void build_kron_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l, const int* l2g);
+void build_band_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l, const int* l2g);
+void build_level_rest(pmg_ctx& c, const pmg_hierarchy_desc& D, int l);
+
 void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   const pmg_level_desc& ld = D.levels[l];
   DevLevel& L = c.lv[l];
@@ -358,6 +368,105 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   const int* l2g_all = ld.l2g;
   const int* l2g = l2g_all + (size_t)c.pb * S;
 
+  if (ld.band_format == PMG_BAND_KRONECKER) {
+    build_kron_level(c, D, l, l2g);
+  } else {
+    build_band_level(c, D, l, l2g);
+  }
+  build_level_rest(c, D, l);
+}
+
+// Matrix-free level (PMG_BAND_KRONECKER): the univariate matrices of the
+// level's free-end space (univariate_mass / univariate_stiffness,
+// spline.cpp:86-110,141-145) and the geometry factors of every local patch.
+void build_kron_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l, const int* l2g) {
+  const pmg_level_desc& ld = D.levels[l];
+  DevLevel& L = c.lv[l];
+  const int d = D.dim, p = D.degree;
+  if (!D.geometry) throw PmgError(PMG_ERR_CONFIG, "the Kronecker operator needs the patch geometry (desc.geometry)");
+  if (!kron_supported(d, p, L.ext))
+    throw PmgError(PMG_ERR_CONFIG, "the Kronecker operator supports degrees 1..8 (2D lines must fit shared memory)");
+  std::vector<double> g(size_t(L.K) * 3, 0.0);
+  for (int k = 0; k < L.K; ++k) {
+    const pmg_patch_geometry& pg = D.geometry[c.pb + k];
+    // x_a = c_a + h_a xi_a  <=>  the control net sits on the Greville abscissae of every axis
+    std::vector<std::vector<double>> grev(d);
+    long long npts = 1;
+    for (int a = 0; a < d; ++a) {
+      const pmg::UnivariateSpace sp(pg.degree[a], pg.elements[a]);
+      const std::vector<double> kn = sp.knots();
+      const int q = pg.degree[a], m = pg.elements[a] + q;
+      grev[a].resize(m);
+      for (int i = 0; i < m; ++i) {
+        double sum = 0.0;
+        for (int j = 1; j <= q; ++j) sum += kn[i + j];
+        grev[a][i] = sum / q;
+      }
+      npts *= m;
+    }
+    double h[3] = {1.0, 1.0, 1.0}, c0[3] = {0.0, 0.0, 0.0}, scale = 0.0;
+    {
+      long long stride = 1;
+      for (int a = 0; a < d; ++a) {
+        const int m = pg.elements[a] + pg.degree[a];
+        c0[a] = pg.ctrl[a];
+        h[a] = pg.ctrl[size_t(stride * (m - 1)) * d + a] - c0[a];
+        scale = std::max(scale, std::fabs(h[a]));
+        stride *= m;
+      }
+    }
+    for (long long f = 0; f < npts; ++f) {
+      long long r = f;
+      for (int a = 0; a < d; ++a) {
+        const int m = pg.elements[a] + pg.degree[a];
+        const int ia = int(r % m);
+        r /= m;
+        if (std::fabs(pg.ctrl[size_t(f) * d + a] - (c0[a] + h[a] * grev[a][ia])) > 1e-13 * scale)
+          throw PmgError(PMG_ERR_CONFIG, "the Kronecker operator needs axis-aligned affine patch maps");
+      }
+    }
+    for (int a = 0; a < d; ++a) {
+      if (!(std::fabs(h[a]) > 1e-14 * scale))
+        throw PmgError(PMG_ERR_GEOMETRY, "the Kronecker operator: degenerate patch map");
+      double v = 1.0 / std::fabs(h[a]);
+      for (int b = 0; b < d; ++b)
+        if (b != a) v *= std::fabs(h[b]);
+      g[size_t(k) * 3 + a] = v;
+    }
+  }
+  const pmg::UnivariateSpace sp(p, ld.elements);
+  const pmg::BandedSymMatrix Mb = pmg::univariate_mass(sp), Kb = pmg::univariate_stiffness(sp);
+  const int W = 2 * p + 1;
+  std::vector<double> M(size_t(L.ext) * W, 0.0), Kst(size_t(L.ext) * W, 0.0);
+  for (int i = 0; i < L.ext; ++i)
+    for (int dl = -p; dl <= p; ++dl) {
+      const int j = i + dl;
+      if (j < 0 || j >= L.ext) continue;
+      M[size_t(i) * W + dl + p] = Mb(i, j);
+      Kst[size_t(i) * W + dl + p] = Kb(i, j);
+    }
+  L.kron = true;
+  L.kron_M = c.upload(M);
+  L.kron_K = c.upload(Kst);
+  L.kron_g = c.upload(g);
+  if (d == 3) L.kron_scratch = c.alloc<double>(size_t(5) * L.lat_n);
+  L.Sp = L.S;
+  L.Ob = L.O;
+  L.l2g = c.upload(l2g, size_t(L.lat_n));
+  {
+    const char* e = std::getenv("PMG_SWEEP");
+    const char* m = std::getenv("PMG_SWEEP_MIN_EXT");
+    c.sweep = (e && e[0] == '0') ? 0 : std::max(1, m ? std::atoi(m) : 128);
+    const char* e3 = std::getenv("PMG_SWEEP3D");
+    c.sweep3 = (e && e[0] == '0') ? 0 : (e3 ? std::atoi(e3) : 30);
+  }
+}
+
+void build_band_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l, const int* l2g) {
+  const pmg_level_desc& ld = D.levels[l];
+  DevLevel& L = c.lv[l];
+  const int d = D.dim, p = D.degree;
+  const long long S = L.S;
   // ---- band: rows of one (patch, offset) pair at stride Sp (>= S, see spmv_row_stride)
   L.Sp = spmv_row_stride(d, p, L.ext, S);
   const long long Sp = L.Sp;
@@ -459,6 +568,16 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
     }
   }
 
+}
+
+void build_level_rest(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
+  const pmg_level_desc& ld = D.levels[l];
+  DevLevel& L = c.lv[l];
+  const int d = D.dim, p = D.degree;
+  const long long S = L.S;
+  const int* l2g_all = ld.l2g;
+  const int* l2g = l2g_all + (size_t)c.pb * S;
+  (void)p;
   // ---- replicas: global owner patch over all patches; local replica CSR
   std::vector<int> owner_patch(size_t(L.N), -1);
   for (int k = 0; k < D.num_patches; ++k)
@@ -680,7 +799,6 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   // factor for the pass form a group whose rows are concatenated (no per-piece
   // row padding); items = (first piece, row panel, column panel, group rows).
   auto make_items = [&](const std::vector<FdPiece>& ps, int naxes, int4** items, int* counts, int* ntcs) {
-    const int BM = fd_rows_per_block();
     for (int pass = 0; pass < 2 * naxes; ++pass) {
       const int axis = pass % naxes, dir = pass / naxes;
       std::vector<std::pair<int, int>> groups;  // (first, count)
@@ -706,11 +824,10 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
         cols.push_back(ps[gr.first].dims[axis]);
         weight.push_back(ps[gr.first].total * gr.second / ps[gr.first].dims[axis]);
       }
-      const char* fntc = std::getenv("PMG_FD_NTC");
-      const int ntc = fntc ? std::atoi(fntc) : fd_pick_ntc(cols.data(), weight.data(), int(groups.size()));
-      if (ntc != 3 && ntc != 5 && ntc != 9 && ntc != 11)
-        throw PmgError(PMG_ERR_CONFIG, "PMG_FD_NTC must be 3, 5, 9 or 11");
-      const int BN = 8 * ntc;
+      const int cfg = fd_pick_cfg(cols.data(), weight.data(), int(groups.size()));
+      if (!fd_cfg_valid(cfg))
+        throw PmgError(PMG_ERR_CONFIG, "no FD kernel for this configuration (PMG_FD_NTC must be 3, 5, 9 or 11)");
+      const int BM = fd_cfg_rows(cfg), BN = fd_cfg_cols(cfg);
       std::vector<int4> it;
       for (const auto& gr : groups) {
         const int K = ps[gr.first].dims[axis];
@@ -721,7 +838,7 @@ void build_level(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
       }
       counts[pass] = int(it.size());
       items[pass] = c.upload(it);
-      ntcs[pass] = ntc;
+      ntcs[pass] = cfg;
     }
   };
   make_items(h_int, d, L.int_items, L.n_int_items, L.int_ntc);
@@ -837,7 +954,7 @@ void build_ctx(pmg_ctx& c, const pmg_hierarchy_desc& D) {
   long long maxlat = 0;
   for (auto& L : c.lv) maxlat = std::max(maxlat, L.lat_n);
   c.partial_n = dot_blocks(maxlat);
-  for (auto& L : c.lv) c.partial_n = std::max(c.partial_n, spmv_partials(c.dim, c.degree, L.S, L.K, L.Ob != L.O, c.sweep, c.sweep3));
+  for (auto& L : c.lv) c.partial_n = std::max(c.partial_n, level_spmv_partials(c, L));
   c.partial = c.alloc<double>(size_t(c.partial_n));
   c.scal = c.alloc<double>(16);
   ck(cudaMemsetAsync(c.scal, 0, 16 * sizeof(double), c.stream), "memset");
@@ -888,8 +1005,25 @@ long long stored_per_patch(int degree, int elements, int dim) {
   return pp;
 }
 
+// dot partials one op_spmv launch of the level writes
+int level_spmv_partials(const pmg_ctx& c, const DevLevel& L) {
+  if (L.kron) return kron_partials(c.dim, c.degree, L.ext, L.S, L.K);
+  return spmv_partials(c.dim, c.degree, L.S, L.K, L.Ob != L.O, c.sweep, c.sweep3);
+}
+
 void op_spmv(pmg_ctx& c, int l, const double* x, const double* f, double* y, double* dot_partial = nullptr) {
   const DevLevel& L = c.lv[l];
+  if (L.kron) {
+    // algorithmic bytes: x, y (and f) plus the 4-byte Dirichlet map per lattice row
+    TimedScope ts(c, 0, l, (8.0 * (f ? 3 : 2) + 4.0) * L.lat_n);
+    KronArgs a{c.dim, c.degree, L.ext, L.S, L.K, L.kron_M, L.kron_K, L.kron_g, L.l2g, x, f, y, dot_partial,
+               L.kron_scratch};
+    int n = 0;
+    launch_kron_spmv(c.stream, a, &n);
+    c.launches += n;
+    c.spmv_launches++;
+    return;
+  }
   // algorithmic bytes: the stored entries of the reference's CSR (harness.cpp:274-282),
   // or with the symmetric half band (stored + diagonal) / 2
   const double entries = double(stored_per_patch(c.degree, L.n, c.dim));
@@ -1244,7 +1378,7 @@ struct PcgParts {
   void front() {
     const DevLevel& F = c.lv[Lf];
     op_spmv(c, Lf, p, nullptr, Ap, c.partial);  // Ap and the partials of Ap.p
-    launch_sum_partials(c.stream, c.partial, spmv_partials(c.dim, c.degree, F.S, F.K, F.Ob != F.O, c.sweep, c.sweep3), s + 1);
+    launch_sum_partials(c.stream, c.partial, level_spmv_partials(c, F), s + 1);
     if (c.multi()) {  // pAp over all ranks, ascending rank order
       c.comm->allgather(c.stream, s + 1, c.rank_buf, 1);
       launch_sum_ranks(c.stream, c.rank_buf, c.size, 1, s + 1);

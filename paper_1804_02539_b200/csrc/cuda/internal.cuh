@@ -114,15 +114,17 @@ enum FdIn { FD_IN_WORK = 0, FD_IN_LATTICE = 1 };
 enum FdOut { FD_OUT_WORK = 0, FD_OUT_WORK_DIAG = 1, FD_OUT_LATTICE_SET = 2, FD_OUT_LATTICE_ADD = 3 };
 
 // One fast-diagonalization pass (contract one axis, rotate the layout).
-// items: (piece, first row, first column, 0) per CTA.
 // items: (first piece of a group of pieces sharing dims and factor, first row
-// of the panel within the group, first column, rows of the group); ntc = the
-// column-panel width in 8-column tiles (fd_pick_ntc)
-void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int ntc, int pass,
+// of the panel within the group, first column, rows of the group) per CTA;
+// cfg = NTC | NW << 8: the column panel in 8-column tiles and the warps (8-row
+// strips) of the CTA (fd_pick_cfg)
+void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int cfg, int pass,
                     int naxes, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
                     const double* work_in, double* work_out);
-int fd_rows_per_block();
-int fd_pick_ntc(const long long* cols, const long long* weight, int n);
+int fd_pick_cfg(const long long* cols, const long long* weight, int n);
+bool fd_cfg_valid(int cfg);
+int fd_cfg_rows(int cfg);  // rows per CTA
+int fd_cfg_cols(int cfg);  // columns per CTA
 void fd_configure();  // per device, before the first pass
 // whole solve of every piece in one launch, one CTA per piece, tensor, diagonal
 // and every factor in shared memory: fd_small_smem(max_total, max_dim, naxes)
@@ -187,6 +189,28 @@ long long spmv_sweep3_band_doubles(int dim, int degree, int ext, long long S, in
                                    int* front, int* e2p);
 void launch_sweep3_relayout(cudaStream_t s, int degree, int ext, long long S, int K, long long Sp, const double* src,
                             double* dst);
+
+// ---------------------------------------------------------------- Kronecker operator
+// Matrix-free operator of a level whose patches are axis-aligned affine
+// (PMG_BAND_KRONECKER, kernels_kron.cu): y = A x or y = f - A x with
+// A = sum_a g[k][a] (x)_{b != a} M (x) K.
+struct KronArgs {
+  int dim, degree, ext;
+  long long S;        // rows per patch
+  int K;              // patches
+  const double* M;    // univariate mass, full band [ext][2p+1] (zero outside the lattice)
+  const double* Kst;  // univariate stiffness, same layout
+  const double* g;    // [K][3] geometry factors
+  const int* l2g;     // [K][S], < 0 on Dirichlet slots
+  const double* x;
+  const double* f;    // residual form; nullptr for y = A x
+  double* y;
+  double* dot_partial;  // optional: per-CTA partials of sum y x (kron_partials of them)
+  double* scratch;      // 3D: 5 lattices
+};
+void launch_kron_spmv(cudaStream_t s, const KronArgs& a, int* launches);
+int kron_partials(int dim, int degree, int ext, long long S, int K);
+bool kron_supported(int dim, int degree, int ext);
 
 // ---------------------------------------------------------------- device PCG loop
 // State of a device-resident pcg_generic loop (multigrid.hpp:155-189): the

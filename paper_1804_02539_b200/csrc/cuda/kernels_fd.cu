@@ -21,6 +21,8 @@
 // thread's copy addresses are computed once per CTA.  Flops per application
 // = sum_pieces 4 prod(m_a) sum(m_a).
 #include <cstdint>
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -30,32 +32,29 @@ namespace pmgcu {
 
 namespace {
 
-constexpr int kFdThreads = 128;
-constexpr int kBM = 32;          // rows per CTA (4 warps x 8)
-#ifndef PMG_FD_BK
-#define PMG_FD_BK 16
-#endif
-#ifndef PMG_FD_MINB
-#define PMG_FD_MINB 4
-#endif
-#ifndef PMG_FD_STAGES
-#define PMG_FD_STAGES 3
-#endif
-constexpr int kBK = PMG_FD_BK;   // k per shared-memory stage
-constexpr int kXS = kBK + 4;     // X row stride (doubles): conflict-free A fragments
-constexpr int kStagesFd = PMG_FD_STAGES;
-constexpr int kXRowStep = kFdThreads / kBK;  // X rows covered by one copy round
+constexpr int kBK = 16;        // k per shared-memory stage
+constexpr int kXS = kBK + 4;   // X row stride (doubles): conflict-free A fragments
 
-// column panel of NTC n-tiles (8 columns each); B row stride = 4 mod 16
-// doubles so the 4 x 8 B-fragment reads of a half-warp hit distinct banks
-template <int NTC, int WM>
+// CTA = NW warps, warp w owns the 8 rows 8w..8w+7 of an 8 NW-row panel and all
+// NTC n-tiles (8 columns each) of the CTA's column panel; K streams through a
+// STAGES-deep cp.async ring.  B row stride = 4 mod 16 doubles so the 4 x 8
+// B-fragment reads of a half-warp hit distinct banks.
+//   <NTC, 4, 3>, 4 CTAs per SM: 32 x 8 NTC tiles, many CTAs (small levels, 3D)
+//   <NTC, 8, 4>, 2 CTAs per SM: 64 x 8 NTC tiles
+//   <NTC, 11, 5>, 1 CTA per SM: 88 x 8 NTC tiles -- at c2's finest level
+//       (4128 rows x 258 columns per pass) 47 x 3 = 141 equal CTAs on 148 SMs,
+//       264 padded columns instead of 288, and 0.39x the L2 -> SM operand bytes
+//       per flop of the 32 x 72 tile
+template <int NTC, int NW, int STAGES>
 struct FdTile {
-  static constexpr int BM = kBM * WM;  // rows per CTA: 4 warps x 8 WM
-  static constexpr int XPer = BM * kBK / kFdThreads;
+  static constexpr int Threads = 32 * NW;
+  static constexpr int BM = 8 * NW;
+  static constexpr int XPer = BM * kBK / Threads;  // = 4
+  static constexpr int XRowStep = Threads / kBK;   // X rows covered by one copy round
   static constexpr int BN = 8 * NTC;
   static constexpr int BS = (BN + 11) / 16 * 16 + 4;
-  static constexpr int BPer = (kBK * BN + kFdThreads - 1) / kFdThreads;
-  static constexpr size_t smem = sizeof(double) * kStagesFd * (BM * kXS + kBK * BS);
+  static constexpr int BPer = (kBK * BN + Threads - 1) / Threads;
+  static constexpr size_t smem = sizeof(double) * STAGES * (BM * kXS + kBK * BS);
 };
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
@@ -129,19 +128,19 @@ __device__ __forceinline__ void fd_epilogue(const FdPiece& P, long long rl, cons
 // (pieces are independent; a group's rows are concatenated so the M
 // dimension has no per-piece padding).  item = (first piece of the group,
 // first row of the panel within the group, first column, rows of the group).
-template <int NTC, int WM>
-__global__ void __launch_bounds__(kFdThreads, WM == 1 ? PMG_FD_MINB : 2) fd_pass_dmma_kernel(const FdPiece* __restrict__ pieces,
-                                                                  const int4* __restrict__ items, int pass,
-                                                                  int naxes, int in_mode, int out_mode,
-                                                                  const double* __restrict__ lat_in,
-                                                                  double* __restrict__ lat_out, double alpha,
-                                                                  const double* __restrict__ work_in,
-                                                                  double* __restrict__ work_out) {
+template <int NTC, int NW, int STAGES, int MINB>
+__global__ void __launch_bounds__(32 * NW, MINB) fd_pass_dmma_kernel(const FdPiece* __restrict__ pieces,
+                                                                     const int4* __restrict__ items, int pass,
+                                                                     int naxes, int in_mode, int out_mode,
+                                                                     const double* __restrict__ lat_in,
+                                                                     double* __restrict__ lat_out, double alpha,
+                                                                     const double* __restrict__ work_in,
+                                                                     double* __restrict__ work_out) {
   PMG_PDL_ENTRY();
-  using T = FdTile<NTC, WM>;
-  extern __shared__ __align__(16) double fd_smem[];  // Xs[kStagesFd][BM * kXS], Bs[kStagesFd][kBK * BS]
+  using T = FdTile<NTC, NW, STAGES>;
+  extern __shared__ __align__(16) double fd_smem[];  // Xs[STAGES][BM * kXS], Bs[STAGES][kBK * BS]
   auto Xs = reinterpret_cast<double(*)[T::BM * kXS]>(fd_smem);
-  auto Bs = reinterpret_cast<double(*)[kBK * T::BS]>(fd_smem + kStagesFd * T::BM * kXS);
+  auto Bs = reinterpret_cast<double(*)[kBK * T::BS]>(fd_smem + STAGES * T::BM * kXS);
   const int4 it = items[blockIdx.x];
   const FdPiece& P0 = pieces[it.x];
   const int axis = pass % naxes;
@@ -157,14 +156,14 @@ __global__ void __launch_bounds__(kFdThreads, WM == 1 ? PMG_FD_MINB : 2) fd_pass
   const double* __restrict__ B = P0.B[axis][dir];
   const int tid = threadIdx.x;
 
-  // per-thread copy plan: X element (rr, kk) = (tid/16 + 8j, tid%16); B element
-  // (kk, nn) of idx = tid + 128j
+  // per-thread copy plan: X element (rr, kk) = (tid/16 + XRowStep j, tid%16); B
+  // element (kk, nn) of idx = tid + Threads j
   const int xk = tid % kBK;
   const double* xsrc[T::XPer];
   bool xrow_ok[T::XPer];
 #pragma unroll
   for (int j = 0; j < T::XPer; ++j) {
-    const long long r = r0 + tid / kBK + kXRowStep * j;
+    const long long r = r0 + tid / kBK + T::XRowStep * j;
     xrow_ok[j] = r < rows;
     const long long rg = xrow_ok[j] ? r : 0;
     const FdPiece& P = pieces[it.x + int(rg / R)];
@@ -178,7 +177,7 @@ __global__ void __launch_bounds__(kFdThreads, WM == 1 ? PMG_FD_MINB : 2) fd_pass
   bool bn_ok[T::BPer];
 #pragma unroll
   for (int j = 0; j < T::BPer; ++j) {
-    const int idx = tid + kFdThreads * j;
+    const int idx = tid + T::Threads * j;
     const int nn = idx % T::BN, kk = idx / T::BN;
     bn_ok[j] = n0 + nn < N && kk < kBK;
     bkk[j] = kk;
@@ -191,7 +190,7 @@ __global__ void __launch_bounds__(kFdThreads, WM == 1 ? PMG_FD_MINB : 2) fd_pass
 #pragma unroll
     for (int j = 0; j < T::XPer; ++j) {
       const bool ok = xrow_ok[j] && k0 + xk < K;
-      cp_async8(xs + (tid / kBK + kXRowStep * j) * kXS + xk, ok ? xsrc[j] + k0 : B, ok);
+      cp_async8(xs + (tid / kBK + T::XRowStep * j) * kXS + xk, ok ? xsrc[j] + k0 : B, ok);
     }
 #pragma unroll
     for (int j = 0; j < T::BPer; ++j) {
@@ -203,54 +202,54 @@ __global__ void __launch_bounds__(kFdThreads, WM == 1 ? PMG_FD_MINB : 2) fd_pass
 
   // epilogues that read global data (the diagonal, or u for u += tau z) pull
   // their lines into L2 now, so the reads after the main loop hit L2: per
-  // column, the panel's 32 rows are 256 contiguous bytes
+  // column, the panel's BM rows are 8 BM contiguous bytes (within one piece)
   if (out_mode == FD_OUT_WORK_DIAG || out_mode == FD_OUT_LATTICE_ADD) {
+    constexpr int LPC = T::BM / 16 + 1;  // 128-byte lines per column
     const long long rl0 = r0 % R;
     const FdPiece& Pf = pieces[it.x + int(r0 / R)];
-    for (int idx = tid; idx < 2 * T::BN; idx += kFdThreads) {
-      const int n = n0 + idx / 2;
+    for (int idx = tid; idx < LPC * T::BN; idx += T::Threads) {
+      const int n = n0 + idx / LPC;
+      const long long dr = min((long long)16 * (idx % LPC), R - 1 - rl0);  // stay inside the piece
       if (n >= N) continue;
       const double* a;
       if (out_mode == FD_OUT_WORK_DIAG) {
-        a = Pf.diag + rl0 + R * n;
+        a = Pf.diag + rl0 + dr + R * n;
       } else {
-        const long long lr = naxes == 3 ? (rl0 % m0) + ext * (rl0 / m0) : rl0;
+        const long long rl = rl0 + dr;
+        const long long lr = naxes == 3 ? (rl % m0) + ext * (rl / m0) : rl;
         a = lat_out + Pf.lat_base + lr + (naxes == 3 ? ext2 : ext) * n;
       }
-      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a + 16 * (idx & 1)));
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a));
     }
   }
 
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  double acc[WM][NTC][2];
+  double acc[NTC][2];
 #pragma unroll
-  for (int u = 0; u < WM; ++u)
-#pragma unroll
-    for (int j = 0; j < NTC; ++j) acc[u][j][0] = acc[u][j][1] = 0.0;
+  for (int j = 0; j < NTC; ++j) acc[j][0] = acc[j][1] = 0.0;
 
   const int nst = (K + kBK - 1) / kBK;
 #pragma unroll
-  for (int s = 0; s < kStagesFd - 1; ++s) {
+  for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nst) load(s, s * kBK);
     cp_async_commit();
   }
   for (int s = 0; s < nst; ++s) {
-    const int cur = s % kStagesFd;
-    cp_async_wait<kStagesFd - 2>();
+    const int cur = s % STAGES;
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
-    {  // prefetch stage s + 2 into the slot freed at s - 1
-      const int nxt = s + kStagesFd - 1;
-      if (nxt < nst) load(nxt % kStagesFd, nxt * kBK);
+    {  // prefetch stage s + STAGES - 1 into the slot freed at s - 1
+      const int nxt = s + STAGES - 1;
+      if (nxt < nst) load(nxt % STAGES, nxt * kBK);
       cp_async_commit();
     }
-    // warp w owns rows 8 WM w .. 8 WM w + 8 WM - 1 of the panel
-    const double* xs = Xs[cur] + (warp * 8 * WM + g) * kXS + t;
+    // warp w owns rows 8 w .. 8 w + 7 of the panel
+    const double* xs = Xs[cur] + (warp * 8 + g) * kXS + t;
     const double* bs = Bs[cur] + t * T::BS + g;
     // fragments of k-step ks + 1 are read while k-step ks multiplies
-    double af[2][WM], bf[2][NTC];
-#pragma unroll
-    for (int u = 0; u < WM; ++u) af[0][u] = xs[u * 8 * kXS];
+    double af[2], bf[2][NTC];
+    af[0] = xs[0];
 #pragma unroll
     for (int j = 0; j < NTC; ++j) bf[0][j] = bs[j * 8];
     // k-steps of 4 that hold rows of B (the last stage of a pass is short)
@@ -260,27 +259,21 @@ __global__ void __launch_bounds__(kFdThreads, WM == 1 ? PMG_FD_MINB : 2) fd_pass
       if (ks >= nks) break;
       const int c = ks & 1;
       if (ks + 1 < kBK / 4) {
-#pragma unroll
-        for (int u = 0; u < WM; ++u) af[c ^ 1][u] = xs[u * 8 * kXS + (ks + 1) * 4];
+        af[c ^ 1] = xs[(ks + 1) * 4];
 #pragma unroll
         for (int j = 0; j < NTC; ++j) bf[c ^ 1][j] = bs[(ks + 1) * 4 * T::BS + j * 8];
       }
 #pragma unroll
-      for (int j = 0; j < NTC; ++j)
-#pragma unroll
-        for (int u = 0; u < WM; ++u) dmma(acc[u][j][0], acc[u][j][1], af[c][u], bf[c][j]);
+      for (int j = 0; j < NTC; ++j) dmma(acc[j][0], acc[j][1], af[c], bf[c][j]);
     }
   }
 
-  // epilogue: lane holds rows r0 + 8 WM w + 8 u + g of the group, columns
+  // epilogue: lane holds row r0 + 8 w + g of the group, columns
   // n0+8j+2t+{0,1}; within its piece, Y(rl, n) at rl + R n
-#pragma unroll
-  for (int u = 0; u < WM; ++u) {
-    const long long r = r0 + warp * 8 * WM + 8 * u + g;
-    if (r >= rows) break;
-    fd_epilogue<NTC>(pieces[it.x + int(r / R)], r % R, acc[u], n0, N, t, naxes, m0, ext, ext2, R, out_mode, alpha,
+  const long long r = r0 + warp * 8 + g;
+  if (r < rows)
+    fd_epilogue<NTC>(pieces[it.x + int(r / R)], r % R, acc, n0, N, t, naxes, m0, ext, ext2, R, out_mode, alpha,
                      lat_out, work_out);
-  }
 }
 
 // ---------------------------------------------------------------- small pieces
@@ -492,23 +485,69 @@ void launch_smooth_small(cudaStream_t s, const SmoothSmallArgs& a, size_t smem) 
   launch_k(smooth_small_kernel, dim3(grid), dim3(kSmallThreads), smem, s, a);
 }
 
+// kernel configurations: cfg = NTC | NW << 8
+#define PMG_FD_CONFIGS(X)                                                                                   \
+  X(3, 4, 3, 4) X(5, 4, 3, 4) X(9, 4, 3, 4) X(11, 4, 3, 4) X(9, 8, 4, 2) X(11, 8, 4, 2) X(9, 11, 5, 1) \
+  X(11, 11, 5, 1)
+
 void fd_configure() {
   ensure_smem((const void*)fd_small_kernel, 200 * 1024);
   ensure_smem((const void*)smooth_small_kernel, 200 * 1024);
-#define PMG_FD_ATTR(NT, W) ensure_smem((const void*)fd_pass_dmma_kernel<NT, W>, FdTile<NT, W>::smem);
-  PMG_FD_ATTR(3, 1) PMG_FD_ATTR(5, 1) PMG_FD_ATTR(9, 1) PMG_FD_ATTR(11, 1) PMG_FD_ATTR(3, 2) PMG_FD_ATTR(5, 2)
-  PMG_FD_ATTR(9, 2) PMG_FD_ATTR(11, 2)
+#define PMG_FD_ATTR(NT, NW, ST, MB) \
+  ensure_smem((const void*)fd_pass_dmma_kernel<NT, NW, ST, MB>, FdTile<NT, NW, ST>::smem);
+  PMG_FD_CONFIGS(PMG_FD_ATTR)
 #undef PMG_FD_ATTR
 }
 
-int fd_wm();
-int fd_rows_per_block() { return kBM * fd_wm(); }
+int fd_cfg_rows(int cfg) { return 8 * (cfg >> 8); }
+int fd_cfg_cols(int cfg) { return 8 * (cfg & 255); }
 
-int fd_pick_ntc(const long long* cols, const long long* weight, int n) {
-  // the column-panel width (in n-tiles) with the least padding over the
-  // groups; 11 (88 columns) is measured slower than 9 at the c2 finest level
-  // (fewer, larger CTAs per wave) and is only used when forced (PMG_FD_NTC).
-  // weight = rows of each group.
+bool fd_cfg_valid(int cfg) {
+#define PMG_FD_VALID(NT, NW, ST, MB) \
+  if (cfg == (NT | NW << 8)) return true;
+  PMG_FD_CONFIGS(PMG_FD_VALID)
+#undef PMG_FD_VALID
+  return false;
+}
+
+int fd_pick_cfg(const long long* cols, const long long* weight, int n) {
+  // PMG_FD_CFG="ntc,nw" forces one configuration; PMG_FD_NTC forces the
+  // column panel of the 4-warp kernel
+  if (const char* e = std::getenv("PMG_FD_CFG")) {
+    int ntc = 0, nw = 0;
+    if (std::sscanf(e, "%d,%d", &ntc, &nw) == 2) return ntc | nw << 8;
+  }
+  if (const char* e = std::getenv("PMG_FD_NTC")) return std::atoi(e) | 4 << 8;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // large passes (every SM gets a full 88-row tile and the contraction is
+  // long enough to amortise the tile's fill and drain): one 11-warp CTA per
+  // SM, with the column panel (72 or 88) that pads N less
+  {
+    static const bool wide_ok = [] {
+      const char* e = std::getenv("PMG_FD_WIDE");
+      return !(e && e[0] == '0');
+    }();
+    long long ctas[2] = {0, 0};
+    double pad[2] = {0.0, 0.0};
+    int kmin = 1 << 30;
+    for (int i = 0; i < n; ++i) {
+      kmin = std::min<long long>(kmin, cols[i]);
+      for (int ci = 0; ci < 2; ++ci) {
+        const int bn = ci ? 88 : 72;
+        const long long cp = (cols[i] + bn - 1) / bn;
+        ctas[ci] += (weight[i] + 87) / 88 * cp;
+        pad[ci] += double((weight[i] + 87) / 88 * 88) * double(cp * bn) * double(cols[i]);
+      }
+    }
+    const int ci = pad[1] <= pad[0] ? 1 : 0;
+    if (wide_ok && kmin >= 192 && ctas[ci] >= (3 * sms) / 4) return (ci ? 11 : 9) | 11 << 8;
+  }
+  // the 4-warp kernel: the column-panel width (in n-tiles) with the least
+  // padding over the groups; 11 (88 columns) is measured slower than 9 at the
+  // c2 finest level (fewer, larger CTAs per wave) and is only used when forced
+  // (PMG_FD_NTC).  weight = rows of each group.
   static const int cands[3] = {3, 5, 9};
   // narrow panels reload A fragments more often per DMMA: measured 0.92x the
   // 72-column rate on c2's finest level for 40 columns
@@ -522,7 +561,7 @@ int fd_pick_ntc(const long long* cols, const long long* weight, int n) {
       const double w = double((cols[i] + 8 * c - 1) / (8 * c) * (8 * c));
       cost[ci] += rate[ci] * double(weight[i]) * w;
       pad[ci] += double(weight[i]) * w;
-      ctas[ci] += (weight[i] + kBM - 1) / kBM * ((cols[i] + 8 * c - 1) / (8 * c));
+      ctas[ci] += (weight[i] + 31) / 32 * ((cols[i] + 8 * c - 1) / (8 * c));
       if (ci == 0) work += double(weight[i]) * double(cols[i]);
     }
   }
@@ -531,38 +570,25 @@ int fd_pick_ntc(const long long* cols, const long long* weight, int n) {
   // a pass that fills fewer than two CTAs per SM is latency-bound: take the
   // panel with the most CTAs among those padding <= 25% (c2 levels 5-6:
   // 8.4 -> 7.3 and 15.5 -> 14 us per pass with 40-column panels, measured)
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (ctas[best] < 2LL * sms)
     for (int ci = 0; ci < 3; ++ci)
       if (pad[ci] <= 1.25 * work && ctas[ci] > ctas[best]) best = ci;
-  return cands[best];
+  return cands[best] | 4 << 8;
 }
 
-int fd_wm() {
-  static const int v = [] {
-    const char* e = std::getenv("PMG_FD_WM");
-    return e && e[0] == '2' ? 2 : 1;
-  }();
-  return v;
-}
-
-void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int ntc, int pass,
+void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int cfg, int pass,
                     int naxes, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
                     const double* work_in, double* work_out) {
   if (nitems == 0) return;
-  const int wm = fd_wm();
-#define PMG_FD_CASE(NT, W)                                                                                     \
-  if (ntc == NT && wm == W) {                                                                                  \
-    launch_k(fd_pass_dmma_kernel<NT, W>, dim3(nitems), dim3(kFdThreads), FdTile<NT, W>::smem, s, pieces, items, \
-             pass, naxes, in_mode, out_mode, lat_in, lat_out, alpha, work_in, work_out);                      \
-    return;                                                                                                    \
+#define PMG_FD_CASE(NT, NW, ST, MB)                                                                             \
+  if (cfg == (NT | NW << 8)) {                                                                                  \
+    launch_k(fd_pass_dmma_kernel<NT, NW, ST, MB>, dim3(nitems), dim3(32 * NW), FdTile<NT, NW, ST>::smem, s, pieces, \
+             items, pass, naxes, in_mode, out_mode, lat_in, lat_out, alpha, work_in, work_out);                 \
+    return;                                                                                                     \
   }
-  PMG_FD_CASE(3, 1) PMG_FD_CASE(5, 1) PMG_FD_CASE(9, 1) PMG_FD_CASE(11, 1) PMG_FD_CASE(3, 2) PMG_FD_CASE(5, 2)
-  PMG_FD_CASE(9, 2) PMG_FD_CASE(11, 2)
+  PMG_FD_CONFIGS(PMG_FD_CASE)
 #undef PMG_FD_CASE
-  throw std::runtime_error("FD pass: no kernel for this column panel (PMG_FD_NTC must be 3, 5, 9 or 11)");
+  throw std::runtime_error("FD pass: no kernel for this configuration (PMG_FD_NTC must be 3, 5, 9 or 11)");
 }
 
 }  // namespace pmgcu

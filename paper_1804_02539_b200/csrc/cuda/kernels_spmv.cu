@@ -1356,7 +1356,10 @@ static bool sweep3_cfg(int dim, int degree, int ext, long long S, int K, bool ha
   const size_t budget = 227 * 1024 - 2048;
   double best = 1e30;
   bool found = false;
+  // experiments: PMG_SWEEP3_TILES / PMG_SWEEP3_ZSEGS pin the in-plane tiles / plane segments
+  static const int pin_tiles = env_int("PMG_SWEEP3_TILES", 0), pin_zsegs = env_int("PMG_SWEEP3_ZSEGS", 0);
   for (int tiles = 1; tiles <= 32; ++tiles) {
+    if (pin_tiles > 0 && tiles != pin_tiles) continue;
     const int T = int((E2 + tiles - 1) / tiles);
     if (T < 96) break;
     const int rpt = (T + kSweep3Nc - 1) / kSweep3Nc;
@@ -1370,6 +1373,7 @@ static bool sweep3_cfg(int dim, int degree, int ext, long long S, int K, bool ha
     const int ns = int(std::min<size_t>(std::min(kSweep3MaxStages, ns_cap),
                                         (budget - xbytes) / (size_t(sd) * sizeof(double))));
     for (int zsegs = 1; zsegs <= 16; ++zsegs) {
+      if (pin_zsegs > 0 && zsegs != pin_zsegs) continue;
       const int zlen = (ext + zsegs - 1) / zsegs;
       if (zlen < 2 * degree) break;
       const int nz = (ext + zlen - 1) / zlen;

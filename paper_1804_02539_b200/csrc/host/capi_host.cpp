@@ -22,6 +22,7 @@ struct pmgh_hierarchy {
   pmgplan::RankPlan plan;  // last pmgh_rank_plan result
   std::vector<std::int32_t> nb_rank, nb_off, nb_iface;
   std::vector<pmg_patch_geometry> geometry;  // empty if a patch map is not describable
+  int flags = 0;                             // PMGH_* build flags
 };
 
 namespace {
@@ -118,6 +119,9 @@ void fill_descriptors(pmgh_hierarchy* H) {
     d.l2g = L.l2g.data();
     d.band_format = L.band.empty() ? PMG_BAND_ASSEMBLE : PMG_BAND_TENSOR;
     d.band = L.band.empty() ? nullptr : L.band.data();
+    // matrix-free levels: the band (when assembled) stays available to host
+    // consumers (the CPU checker); the CUDA context does not read it
+    if ((H->flags & PMGH_KRONECKER) && l >= 1) d.band_format = PMG_BAND_KRONECKER;
     if (l >= 1) {
       const TwoScaleMatrix& P = L.two_scale;
       d.ts_fine_dim = P.fine_dim;
@@ -227,6 +231,7 @@ int pmgh_build_ex(const char* domain, int split, int degree, int n0, int levels,
     H->h = std::make_unique<Hierarchy>(dom, degree, n0, levels, cp, rs, threads,
                                        (flags & PMGH_DEVICE_ASSEMBLY) == 0);
     if ((flags & PMGH_DEVICE_ASSEMBLY) && dom.patches.empty()) throw ConfigError("pmgh_build: no patches");
+    H->flags = flags;
     fill_descriptors(H.get());
     *out = H.release();
   });

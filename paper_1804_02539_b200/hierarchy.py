@@ -35,21 +35,31 @@ class Hierarchy:
     assembly="device" leaves the stiffness of levels >= 1 unassembled on the
     host: a GpuBackend context assembles it on the B200 from the patch
     geometry (PMG_BAND_ASSEMBLE).  Such a hierarchy has no host band to give
-    the oracle; tests pair it with a host-assembled twin."""
+    the oracle; tests pair it with a host-assembled twin.
+
+    operator="kronecker" describes levels >= 1 as PMG_BAND_KRONECKER: the
+    context applies the patch operator matrix-free as a Kronecker sum of
+    univariate matrices (axis-aligned affine patch maps only: c1, c3,
+    unit_grid, lshape, fichera ...).  The host band stays available to the
+    oracle."""
 
     def __init__(self, domain: str, degree: int, levels: int, n0: int = 1, split: int = 1,
                  params: CycleParams | None = None, rhs: str = "default", seed: int = 42,
-                 threads: int | None = None, assembly: str = "host"):
+                 threads: int | None = None, assembly: str = "host", operator: str = "band"):
         if assembly not in ("host", "device"):
             raise ValueError("assembly must be 'host' or 'device'")
+        if operator not in ("band", "kronecker"):
+            raise ValueError("operator must be 'band' or 'kronecker'")
         self.assembly = assembly
+        self.operator = operator
         lib = N.host_lib()
         self.params = params or CycleParams()
         self.domain = domain
         self.seed = seed
         self.threads = threads or os.cpu_count() or 1
         h = C.c_void_p()
-        flags = N.PMGH_DEVICE_ASSEMBLY if assembly == "device" else 0
+        flags = (N.PMGH_DEVICE_ASSEMBLY if assembly == "device" else 0) | (
+            N.PMGH_KRONECKER if operator == "kronecker" else 0)
         rc = lib.pmgh_build_ex(domain.encode(), split, degree, n0, levels, C.byref(self.params.to_c()),
                                RHS_KINDS[rhs], seed, self.threads, flags, C.byref(h))
         raise_for(rc, lib.pmgh_last_error().decode())
@@ -100,7 +110,8 @@ class Hierarchy:
         return np.ctypeslib.as_array(self.desc.levels[level].l2g, shape=(n,)).reshape(self.num_patches, -1)
 
     def band(self, level: int) -> np.ndarray:
-        if self.desc.levels[level].band_format != N.PMG_BAND_TENSOR:
+        if self.desc.levels[level].band_format not in (N.PMG_BAND_TENSOR, N.PMG_BAND_KRONECKER) or not \
+                self.desc.levels[level].band:
             raise ValueError(f"level {level} is assembled on the device; no host band")
         o = (2 * self.degree + 1) ** self.dim
         s = self.lattice_size(level)

@@ -338,3 +338,32 @@ def test_plane_sweep_matches_tma_half(dom, p, lv, n0, min_ext, monkeypatch):
         assert rel(out[min_ext][0][level][1], ref.residual(level, f, u)) < 1e-13
     assert out[min_ext][2] == out["0"][2]
     assert rel(out[min_ext][1], out["0"][1]) < 1e-10
+
+
+@pytest.mark.parametrize("dom,p,lv,n0,rhs", [("lshape", 2, 3, 1, "one"), ("c2", 4, 4, 2, "default"),
+                                             ("c4", 3, 3, 2, "default"), ("fichera", 2, 3, 1, "sine3d")])
+@pytest.mark.parametrize("prm", [dict(mu=2), dict(nu=2), dict(mu=2, nu=2, damp_coarse=True), dict(tau=0.2)],
+                         ids=["W", "V22", "W22damp", "tau"])
+def test_cycle_parameters_match_oracle(dom, p, lv, n0, rhs, prm):
+    """Non-default CycleParams (multigrid.hpp:21-27) on the device cycle: the
+    W-cycle mu = 2 (multigrid.hpp:134, the recursion runs twice per level from
+    the second visit's non-zero coarse iterate), nu = 2 pre/post smoothing
+    steps, damp_coarse and another tau -- fused cycle, preconditioner and the
+    full PCG against the oracle; test_multigrid.cpp:291-310 is the reference's
+    own W-cycle check."""
+    from paper_1804_02539_b200.hierarchy import CycleParams
+    h = Hierarchy(dom, p, lv, n0=n0, rhs=rhs, params=CycleParams(**prm))
+    b, o = GpuBackend(h), oracle.Oracle(h)
+    L = h.finest_level
+    f = rand(h.num_dofs(L), 3)
+    u = rand(h.num_dofs(L), 4)
+    ug = b.to_accumulated(L, u)
+    b.mg_cycle(L, ug, b.to_distributed_owner(L, f))
+    assert rel(b.gather_global(L, ug), o.mg_cycle(L, u, f)) < 1e-11
+    z = b.gather_global(L, b.precondition(b.to_distributed_owner(L, f)))
+    assert rel(z, o.precondition(f)) < 1e-11
+    fr = h.rhs()
+    u_ref, hist_ref, _, _ = o.pcg_solve(fr)
+    us, rep = b.pcg_solve(fr)
+    assert rep.iterations == len(hist_ref) - 1
+    assert rel(us, u_ref) < 1e-10
