@@ -528,6 +528,20 @@ def main():
                         "value read once from HBM and used as lower and mirrored upper entry from shared memory)")
                        + ", finest level; bytes = half band 8 (S + D) / 2 + 8 B per lattice row for x, y (and f), "
                          "SURVEY.md 8(d), DESIGN.md 3")
+    # per level: launches and ms per step of every timed class, and the SpMV's
+    # fraction of the HBM peak on its algorithmic bytes
+    per_level = {}
+    for lv in levels:
+        row = {}
+        for c in range(6):
+            nl_, t_, w_ = per[(c, lv)]
+            if nl_:
+                row[names[c]] = {"launches_per_step": nl_ / steps, "ms_per_step": t_ / steps}
+                if c == 0 and t_ > 0:
+                    row[names[c]]["hbm_frac"] = (w_ / (t_ / 1e3) / 1e9) / hbm
+                if c == 1 and t_ > 0:
+                    row[names[c]]["tflops"] = w_ / (t_ / 1e3) / 1e12
+        per_level[str(lv)] = row
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
         "frac": (achieved / hbm) if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
@@ -542,6 +556,7 @@ def main():
                       "peak_source": "measured DMMA m8n8k4 peak on a B200, profiles/fp64_peak_r01.txt",
                       "share_of_step": fd_ms / steps / ms_step},
         "breakdown": breakdown,
+        "per_level": per_level,
     }
     vcycle = {
         "ms": v_ms, "t_roof_ms": t_roof_ms, "frac": t_roof_ms / v_ms,

@@ -829,7 +829,17 @@ void build_level_rest(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
         throw PmgError(PMG_ERR_CONFIG, "no FD kernel for this configuration (PMG_FD_NTC must be 3, 5, 9 or 11)");
       const int BM = fd_cfg_rows(cfg), BN = fd_cfg_cols(cfg);
       std::vector<int4> it;
+      if (fd_cfg_resident(cfg)) {
+        std::vector<std::pair<int, long long>> gl;
+        for (const auto& gr : groups) {
+          const long long rows = ps[gr.first].total / ps[gr.first].dims[axis] * gr.second;
+          if (rows > INT32_MAX) throw PmgError(PMG_ERR_CONFIG, "FD piece group too large");
+          gl.push_back({gr.first, rows});
+        }
+        fd_resident_items(gl, it);
+      }
       for (const auto& gr : groups) {
+        if (fd_cfg_resident(cfg)) break;
         const int K = ps[gr.first].dims[axis];
         const long long rows = ps[gr.first].total / K * gr.second;
         if (rows > INT32_MAX) throw PmgError(PMG_ERR_CONFIG, "FD piece group too large");

@@ -123,6 +123,11 @@ void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, in
                     const double* work_in, double* work_out);
 int fd_pick_cfg(const long long* cols, const long long* weight, int n);
 bool fd_cfg_valid(int cfg);
+// cfg | kFdResident: the resident-factor kernel for short contractions
+// (K = N <= 88, many rows); its items come from fd_resident_items
+constexpr int kFdResident = 1 << 16;
+bool fd_cfg_resident(int cfg);
+void fd_resident_items(const std::vector<std::pair<int, long long>>& groups, std::vector<int4>& items);
 int fd_cfg_rows(int cfg);  // rows per CTA
 int fd_cfg_cols(int cfg);  // columns per CTA
 void fd_configure();  // per device, before the first pass

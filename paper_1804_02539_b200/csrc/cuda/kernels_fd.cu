@@ -24,6 +24,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <utility>
+#include <vector>
 
 #include "internal.cuh"
 #include "pieces.cuh"
@@ -276,6 +278,212 @@ __global__ void __launch_bounds__(32 * NW, MINB) fd_pass_dmma_kernel(const FdPie
                      lat_out, work_out);
 }
 
+// ---------------------------------------------------------------- short contractions
+// Passes with K = N <= 8 NTC (the 3D levels: c4/c5 contract 65-67 entries):
+// the factor stays resident.  One persistent CTA per SM loads B once; each of
+// its kResWarps warps then works alone -- it takes the next 8-row strip of
+// the CTA's range from a shared counter, copies the strip's X rows into its
+// own double buffer with cp.async while the previous strip multiplies, runs
+// ceil(K / 4) k-steps of NTC DMMAs from shared memory, and stores.  No
+// CTA-wide barrier after the prologue, no per-tile pipeline fill.
+// item = (first piece of the group, first strip, end strip, rows of the
+// group): the CTAs of a group split its strips evenly (fd_resident_items).
+constexpr int kResWarps = 12;
+
+// Row of a group as a warp lane sees it: the piece it lies in, its row there,
+// and where that row's input starts / its output goes.  All patch-local
+// indices fit 32 bits (a rank's lattice has < 2^31 slots), so the per-strip
+// index arithmetic is 32-bit: with 64-bit divisions the strip's ~150 DMMAs
+// were outnumbered 10:1 by integer instructions and the pass was issue-bound.
+struct ResRow {
+  const double* src;  // first input element of the row
+  double* dst;        // output element (row, column 0)
+  const double* aux;  // diagonal (FD_OUT_WORK_DIAG) or nothing
+};
+
+template <int NTC>
+__global__ void __launch_bounds__(32 * kResWarps, 1) fd_pass_resident_kernel(
+    const FdPiece* __restrict__ pieces, const int4* __restrict__ items, int pass, int naxes, int in_mode,
+    int out_mode, const double* __restrict__ lat_in, double* __restrict__ lat_out, double alpha,
+    const double* __restrict__ work_in, double* __restrict__ work_out) {
+  PMG_PDL_ENTRY();
+  constexpr int BN = 8 * NTC;
+  constexpr int BS = (BN + 11) / 16 * 16 + 4;  // = 4 mod 16: conflict-free B fragments
+  extern __shared__ __align__(16) double fd_smem[];
+  __shared__ int next_strip;
+  const int4 it = items[blockIdx.x];
+  const FdPiece& P0 = pieces[it.x];
+  const int axis = pass % naxes, dir = pass / naxes;
+  const int K = P0.dims[axis];
+  const int N = K;
+  const int nks = (K + 3) / 4;
+  const int Kp = 4 * nks;
+  const int XS = (Kp & 7) == 4 ? Kp : Kp + 4;  // = 4 mod 8: conflict-free A fragments
+  const int R = int(P0.total / K);             // rows per piece
+  const int rows = it.w;
+  const int m0 = P0.dims[0], m1 = P0.dims[1];
+  const int ext = P0.ext, ext2 = P0.ext * P0.ext;
+  const int ostride = out_mode >= FD_OUT_LATTICE_SET ? (naxes == 3 ? ext2 : ext) : R;  // output column stride
+  const double* __restrict__ B = P0.B[axis][dir];
+  double* Bs = fd_smem;                 // [Kp][BS], zero outside K x N
+  double* Xall = Bs + (size_t)Kp * BS;  // [kResWarps][2][8][XS]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+
+  if (tid == 0) next_strip = it.y;
+  for (int idx = tid; idx < Kp * BS; idx += 32 * kResWarps) {
+    const int kk = idx / BS, nn = idx - kk * BS;
+    const bool ok = kk < K && nn < N;
+    cp_async8(Bs + idx, ok ? B + kk * N + nn : B, ok);
+  }
+  cp_async_commit();
+  double* Xw = Xall + (size_t)warp * 2 * 8 * XS;
+  for (int idx = lane; idx < 2 * 8 * XS; idx += 32) Xw[idx] = 0.0;  // the columns >= K stay zero
+  __syncthreads();
+
+  // lane (g, t) owns row g of a strip: it copies the row's elements t, t + 4,
+  // ... and stores the row's outputs of columns 8 j + 2 t + {0, 1}
+  auto locate = [&](int strip) {
+    int r = strip * 8 + g;
+    if (r >= rows) r = rows - 1;  // a short last strip repeats its last row (never stored)
+    const int pi = r / R, rl = r - pi * R;
+    const FdPiece& P = pieces[it.x + pi];
+    ResRow w;
+    if (in_mode == FD_IN_WORK) {
+      w.src = work_in + P.work_off + (long long)rl * K;
+    } else {
+      const int i2 = naxes == 3 ? rl / m1 : 0, i1 = naxes == 3 ? rl - i2 * m1 : rl;
+      w.src = lat_in + P.lat_base + (ext * i1 + ext2 * i2);
+    }
+    if (out_mode >= FD_OUT_LATTICE_SET) {
+      const int j1 = naxes == 3 ? rl / m0 : 0, j0 = naxes == 3 ? rl - j1 * m0 : rl;
+      w.dst = lat_out + P.lat_base + (j0 + ext * j1);
+    } else {
+      w.dst = work_out + P.work_off + rl;
+    }
+    w.aux = P.diag + rl;
+    return w;
+  };
+  auto issue = [&](const ResRow& w, double* xb) {
+    double* dst = xb + g * XS + t;
+    const double* src = w.src + t;
+    for (int k = t; k < K; k += 4, dst += 4, src += 4) cp_async8(dst, src, true);
+  };
+  auto grab = [&]() {
+    int s = 0;
+    if (lane == 0) s = atomicAdd(&next_strip, 1);
+    return __shfl_sync(0xffffffffu, s, 0);
+  };
+
+  int cur = grab();
+  ResRow wc = locate(cur < it.z ? cur : it.y);
+  if (cur < it.z) issue(wc, Xw);
+  cp_async_commit();
+  int buf = 0;
+  while (cur < it.z) {
+    const int nxt = grab();
+    ResRow wn = wc;
+    if (nxt < it.z) {
+      wn = locate(nxt);
+      issue(wn, Xw + (buf ^ 1) * 8 * XS);
+    }
+    cp_async_commit();
+    // epilogues that read global data pull their lines into L2 during the
+    // products: per column the strip's 8 rows are 64 contiguous bytes
+    if (out_mode == FD_OUT_WORK_DIAG || out_mode == FD_OUT_LATTICE_ADD) {
+      const double* a0 = out_mode == FD_OUT_WORK_DIAG ? wc.aux : wc.dst;
+      if (g == 0 || g == 7)  // first and last row: both lines a misaligned strip touches
+        for (int n = t; n < N; n += 4) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a0 + (long long)ostride * n));
+    }
+    cp_async_wait<1>();  // the current strip (and, the first time, B) has landed
+    __syncwarp();
+    const double* xs = Xw + buf * 8 * XS + g * XS + t;
+    const double* bs = Bs + t * BS + g;
+    double acc[NTC][2];
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) acc[j][0] = acc[j][1] = 0.0;
+    // k-steps in pairs over two named fragment sets (static register names:
+    // a [2][NTC] array indexed by ks & 1 lands in local memory); the fragments
+    // of the next k-step are read while the current one multiplies
+    double a0 = xs[0], a1 = 0.0, b0[NTC], b1[NTC];
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) b0[j] = bs[j * 8];
+    int ks = 0;
+    for (; ks + 1 < nks; ks += 2) {
+      a1 = xs[(ks + 1) * 4];
+#pragma unroll
+      for (int j = 0; j < NTC; ++j) b1[j] = bs[(ks + 1) * 4 * BS + j * 8];
+#pragma unroll
+      for (int j = 0; j < NTC; ++j) dmma(acc[j][0], acc[j][1], a0, b0[j]);
+      if (ks + 2 < nks) {
+        a0 = xs[(ks + 2) * 4];
+#pragma unroll
+        for (int j = 0; j < NTC; ++j) b0[j] = bs[(ks + 2) * 4 * BS + j * 8];
+      }
+#pragma unroll
+      for (int j = 0; j < NTC; ++j) dmma(acc[j][0], acc[j][1], a1, b1[j]);
+    }
+    if (ks < nks) {
+#pragma unroll
+      for (int j = 0; j < NTC; ++j) dmma(acc[j][0], acc[j][1], a0, b0[j]);
+    }
+    if (cur * 8 + g < rows) {
+      // Y(row, n) at dst + ostride n, n = 8 j + 2 t + i
+      double* o = wc.dst + (long long)ostride * (2 * t);
+      const long long step = (long long)ostride * 8;
+      if (out_mode == FD_OUT_WORK) {
+#pragma unroll
+        for (int j = 0; j < NTC; ++j, o += step) {
+          const int n = 8 * j + 2 * t;
+          if (n < N) o[0] = acc[j][0];
+          if (n + 1 < N) o[ostride] = acc[j][1];
+        }
+      } else if (out_mode == FD_OUT_LATTICE_SET) {
+#pragma unroll
+        for (int j = 0; j < NTC; ++j, o += step) {
+          const int n = 8 * j + 2 * t;
+          if (n < N) o[0] = alpha * acc[j][0];
+          if (n + 1 < N) o[ostride] = alpha * acc[j][1];
+        }
+      } else {
+        // all loads first (one round trip), then the stores
+        const double* q = (out_mode == FD_OUT_WORK_DIAG ? wc.aux : wc.dst) + (long long)ostride * (2 * t);
+        double ld[NTC][2];
+#pragma unroll
+        for (int j = 0; j < NTC; ++j) {
+          const int n = 8 * j + 2 * t;
+          ld[j][0] = n < N ? q[step * j] : 1.0;
+          ld[j][1] = n + 1 < N ? q[step * j + ostride] : 1.0;
+        }
+#pragma unroll
+        for (int j = 0; j < NTC; ++j, o += step) {
+          const int n = 8 * j + 2 * t;
+          if (out_mode == FD_OUT_WORK_DIAG) {
+            if (n < N) o[0] = acc[j][0] / ld[j][0];
+            if (n + 1 < N) o[ostride] = acc[j][1] / ld[j][1];
+          } else {
+            if (n < N) o[0] = ld[j][0] + alpha * acc[j][0];
+            if (n + 1 < N) o[ostride] = ld[j][1] + alpha * acc[j][1];
+          }
+        }
+      }
+    }
+    __syncwarp();  // every lane is done with this buffer before the next copy into it
+    cur = nxt;
+    wc = wn;
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
+template <int NTC>
+size_t fd_resident_smem(int K) {
+  const int Kp = (K + 3) / 4 * 4;
+  const int XS = (Kp & 7) == 4 ? Kp : Kp + 4;
+  const int BS = (8 * NTC + 11) / 16 * 16 + 4;
+  return sizeof(double) * (size_t(Kp) * BS + size_t(kResWarps) * 2 * 8 * XS);
+}
+
 // ---------------------------------------------------------------- small pieces
 // Pieces that fit in shared memory (coarse levels): one CTA runs the whole
 // solve -- gather from the lattice (or a work buffer), d forward products,
@@ -497,12 +705,55 @@ void fd_configure() {
   ensure_smem((const void*)fd_pass_dmma_kernel<NT, NW, ST, MB>, FdTile<NT, NW, ST>::smem);
   PMG_FD_CONFIGS(PMG_FD_ATTR)
 #undef PMG_FD_ATTR
+  ensure_smem((const void*)fd_pass_resident_kernel<9>, fd_resident_smem<9>(72));
+  ensure_smem((const void*)fd_pass_resident_kernel<11>, fd_resident_smem<11>(88));
 }
 
-int fd_cfg_rows(int cfg) { return 8 * (cfg >> 8); }
+// CTA items of the resident-factor kernel: the SMs are shared out over the
+// groups in proportion to their strips (every group at least one CTA), and a
+// group's CTAs split its strips evenly.  groups: (first piece, rows).
+void fd_resident_items(const std::vector<std::pair<int, long long>>& groups, std::vector<int4>& items) {
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long total = 0;
+  for (const auto& gr : groups) total += (gr.second + 7) / 8;
+  int left = sms - int(groups.size());
+  std::vector<int> ctas(groups.size(), 1);
+  std::vector<double> want(groups.size());
+  for (size_t i = 0; i < groups.size(); ++i) {
+    want[i] = double((groups[i].second + 7) / 8) * sms / double(total);
+    const int extra = std::max(0, std::min(left, int(want[i]) - 1));
+    ctas[i] += extra;
+    left -= extra;
+  }
+  // the SMs left by rounding go to the groups with the most strips per CTA
+  while (left > 0) {
+    size_t b = 0;
+    double worst = -1.0;
+    for (size_t i = 0; i < groups.size(); ++i) {
+      const double load = double((groups[i].second + 7) / 8) / ctas[i];
+      if (load > worst) worst = load, b = i;
+    }
+    ctas[b]++;
+    left--;
+  }
+  for (size_t i = 0; i < groups.size(); ++i) {
+    const long long strips = (groups[i].second + 7) / 8;
+    const int nc = int(std::min<long long>(ctas[i], strips));
+    for (int j = 0; j < nc; ++j)
+      items.push_back(make_int4(groups[i].first, int(strips * j / nc), int(strips * (j + 1) / nc),
+                                int(groups[i].second)));
+  }
+}
+
+// cfg with kFdResident set: fd_pass_resident_kernel<NTC> (persistent CTAs, resident factor)
+bool fd_cfg_resident(int cfg) { return (cfg & kFdResident) != 0; }
+int fd_cfg_rows(int cfg) { return 8 * ((cfg >> 8) & 255); }
 int fd_cfg_cols(int cfg) { return 8 * (cfg & 255); }
 
 bool fd_cfg_valid(int cfg) {
+  if (fd_cfg_resident(cfg)) return (cfg & 255) == 9 || (cfg & 255) == 11;
 #define PMG_FD_VALID(NT, NW, ST, MB) \
   if (cfg == (NT | NW << 8)) return true;
   PMG_FD_CONFIGS(PMG_FD_VALID)
@@ -515,12 +766,33 @@ int fd_pick_cfg(const long long* cols, const long long* weight, int n) {
   // column panel of the 4-warp kernel
   if (const char* e = std::getenv("PMG_FD_CFG")) {
     int ntc = 0, nw = 0;
-    if (std::sscanf(e, "%d,%d", &ntc, &nw) == 2) return ntc | nw << 8;
+    if (std::sscanf(e, "%d,%d", &ntc, &nw) == 2) {
+      if (nw != 0) return ntc | nw << 8;
+      // "ntc,0": the resident-factor kernel where the contraction fits, else the default
+      int kmax = 0;
+      for (int i = 0; i < n; ++i) kmax = std::max<long long>(kmax, cols[i]);
+      if (kmax <= 8 * ntc && n <= 148) return ntc | kFdResident;
+    }
   }
   if (const char* e = std::getenv("PMG_FD_NTC")) return std::atoi(e) | 4 << 8;
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // short contractions with many rows (3D levels): the resident-factor kernel
+  {
+    static const bool res_ok = [] {
+      const char* e = std::getenv("PMG_FD_RESIDENT");
+      return !(e && e[0] == '0');
+    }();
+    int kmax = 0;
+    long long strips = 0;
+    for (int i = 0; i < n; ++i) {
+      kmax = std::max<long long>(kmax, cols[i]);
+      strips += (weight[i] + 7) / 8;
+    }
+    if (res_ok && kmax <= 88 && kmax >= 24 && strips >= 2LL * sms * kResWarps && n <= sms)
+      return (kmax <= 72 ? 9 : 11) | kFdResident;
+  }
   // large passes (every SM gets a full 88-row tile and the contraction is
   // long enough to amortise the tile's fill and drain): one 11-warp CTA per
   // SM, with the column panel (72 or 88) that pads N less
@@ -580,6 +852,17 @@ void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, in
                     int naxes, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
                     const double* work_in, double* work_out) {
   if (nitems == 0) return;
+  if (fd_cfg_resident(cfg)) {
+    // one smem size per launch: the largest contraction the kernel may see is 8 NTC
+    if ((cfg & 255) == 9) {
+      launch_k(fd_pass_resident_kernel<9>, dim3(nitems), dim3(32 * kResWarps), fd_resident_smem<9>(72), s, pieces,
+               items, pass, naxes, in_mode, out_mode, lat_in, lat_out, alpha, work_in, work_out);
+    } else {
+      launch_k(fd_pass_resident_kernel<11>, dim3(nitems), dim3(32 * kResWarps), fd_resident_smem<11>(88), s, pieces,
+               items, pass, naxes, in_mode, out_mode, lat_in, lat_out, alpha, work_in, work_out);
+    }
+    return;
+  }
 #define PMG_FD_CASE(NT, NW, ST, MB)                                                                             \
   if (cfg == (NT | NW << 8)) {                                                                                  \
     launch_k(fd_pass_dmma_kernel<NT, NW, ST, MB>, dim3(nitems), dim3(32 * NW), FdTile<NT, NW, ST>::smem, s, pieces, \

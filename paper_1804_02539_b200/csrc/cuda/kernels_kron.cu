@@ -197,16 +197,21 @@ size_t kron2d_smem(int p, int E, int TL) {
 
 }  // namespace
 
-int kron2d_lines(int p, int ext) {
-  // lines per CTA: as many as fit 160 KB, at most 32 (halo overhead 2p / TL)
+int kron2d_lines(int p, int ext, int K) {
+  // lines per CTA: 32 (the axis-0 sweep of the 2p halo lines is recomputed by
+  // the neighbouring CTA), 16 when that leaves most SMs without a CTA
+  // (measured at c3p8, 16 patches of 136 lines: 25 us with 32 lines on 80 CTAs;
+  // 8 lines on 272 CTAs with M, K through L1: 47 us); fewer if the tile
+  // exceeds shared memory
   int tl = 32;
-  while (tl > 1 && kron2d_smem(p, ext, tl) > 160 * 1024) tl /= 2;
+  if ((long long)K * ((ext + 31) / 32) < 120) tl = 16;
+  while (tl > 1 && kron2d_smem(p, ext, tl) > 200 * 1024) tl /= 2;
   return kron2d_smem(p, ext, tl) <= 200 * 1024 ? tl : 0;
 }
 
 int kron_partials(int dim, int degree, int ext, long long S, int K) {
   if (dim == 2) {
-    const int tl = kron2d_lines(degree, ext);
+    const int tl = kron2d_lines(degree, ext, K);
     return K * ((ext + tl - 1) / tl);
   }
   return int((S * K + kKronThreads - 1) / kKronThreads);
@@ -214,7 +219,7 @@ int kron_partials(int dim, int degree, int ext, long long S, int K) {
 
 bool kron_supported(int dim, int degree, int ext) {
   if (degree < 1 || degree > 8) return false;
-  return dim == 3 || (dim == 2 && kron2d_lines(degree, ext) > 0);
+  return dim == 3 || (dim == 2 && kron2d_lines(degree, ext, 1 << 20) > 0);
 }
 
 void launch_kron_spmv(cudaStream_t s, const KronArgs& a, int* launches) {
@@ -223,7 +228,7 @@ void launch_kron_spmv(cudaStream_t s, const KronArgs& a, int* launches) {
 #define PMG_KRON_CASE(PP)                                                                                         \
   case PP:                                                                                                        \
     if (a.dim == 2) {                                                                                             \
-      const int tl = kron2d_lines(PP, a.ext);                                                                     \
+      const int tl = kron2d_lines(PP, a.ext, a.K);                                                                     \
       const size_t smem = kron2d_smem(PP, a.ext, tl);                                                             \
       ensure_smem((const void*)kron2d_kernel<PP>, smem);                                                          \
       launch_k(kron2d_kernel<PP>, dim3(a.K * ((a.ext + tl - 1) / tl)), dim3(kKronThreads), smem, s, a, tl);       \

@@ -1357,7 +1357,10 @@ static bool sweep3_cfg(int dim, int degree, int ext, long long S, int K, bool ha
   double best = 1e30;
   bool found = false;
   // experiments: PMG_SWEEP3_TILES / PMG_SWEEP3_ZSEGS pin the in-plane tiles / plane segments
-  static const int pin_tiles = env_int("PMG_SWEEP3_TILES", 0), pin_zsegs = env_int("PMG_SWEEP3_ZSEGS", 0);
+  // (levels with ext >= 48; PMG_SWEEP3_TILES_C / PMG_SWEEP3_ZSEGS_C the coarser ones)
+  static const int pin_t = env_int("PMG_SWEEP3_TILES", 0), pin_z = env_int("PMG_SWEEP3_ZSEGS", 0);
+  static const int pin_tc = env_int("PMG_SWEEP3_TILES_C", 0), pin_zc = env_int("PMG_SWEEP3_ZSEGS_C", 0);
+  const int pin_tiles = ext >= 48 ? pin_t : pin_tc, pin_zsegs = ext >= 48 ? pin_z : pin_zc;
   for (int tiles = 1; tiles <= 32; ++tiles) {
     if (pin_tiles > 0 && tiles != pin_tiles) continue;
     const int T = int((E2 + tiles - 1) / tiles);
@@ -1380,7 +1383,10 @@ static bool sweep3_cfg(int dim, int degree, int ext, long long S, int K, bool ha
       const long long ctas = (long long)K * tiles * nz;
       if (ctas > sms) break;  // one wave: CTAs run start to end
       const double fill = std::min(1.0, double(ctas) / (0.9 * sms));
-      const double cost = (double(tpad) / T + 0.5 * H / T) * (1.0 + (nz > 1 ? 1.7 / zlen : 0.0)) / fill;
+      // fitted to c4's finest level (K = 8, ext = 67; tiles x segments, ms per launch): 3 x 6 0.598,
+      // 4 x 4 0.668, 6 x 3 0.849, 4 x 3 0.869, 9 x 2 1.183, 12 x 1 2.150 -- the in-plane halo costs about
+      // twice its rows (band rows and x window re-read by the neighbouring tile, shorter bulk copies)
+      const double cost = (double(tpad) / T + 2.0 * H / T) * (1.0 + (nz > 1 ? 1.7 / zlen : 0.0)) / fill;
       if (cost < best) {
         best = cost;
         found = true;
@@ -1400,7 +1406,12 @@ static bool sweep3_cfg(int dim, int degree, int ext, long long S, int K, bool ha
       }
     }
   }
-  return found;
+  // a level whose best sweep still re-reads or idles this much (few patches
+  // of a small lattice: c4 level 4 ran at 0.18 of HBM, c5 level 4 at 0.57) is
+  // served as well or better by the 256-row half-band kernel (0.58 at c5 level 4)
+  // (an explicit PMG_SWEEP3D threshold -- the parity tests -- sweeps every level that qualifies)
+  static const int cost_cap = env_int("PMG_SWEEP3_COST_PCT", std::getenv("PMG_SWEEP3D") ? 1000000 : 170);
+  return found && best <= 0.01 * cost_cap;
 }
 
 template <int P>

@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -437,12 +439,16 @@ Hierarchy::Hierarchy(const MultiPatchDomain& domain, int degree, int n0, int lev
   const int K = domain_->num_patches();
 
   auto t0 = std::chrono::steady_clock::now();
+  const bool timing = std::getenv("PMG_SETUP_TIMING") != nullptr;
+  double t_map = 0, t_cls = 0, t_pay = 0;
   levels_.resize(levels + 1);
   EigCache cache;
   for (int l = 0; l <= levels; ++l) {
     Level& L = levels_[l];
     L.elements = n0 << l;
+    auto ta = std::chrono::steady_clock::now();
     L.mapper = std::make_unique<DofMapper>(*domain_, degree, L.elements);
+    t_map += seconds_since(ta);
     const std::int64_t S = L.mapper->lattice_size();
     L.l2g.resize(std::size_t(S) * K);
     for (int k = 0; k < K; ++k)
@@ -451,7 +457,10 @@ Hierarchy::Hierarchy(const MultiPatchDomain& domain, int degree, int n0, int lev
     // smoother pieces and payloads (smoother.cpp:84-108)
     const double h = 1.0 / L.elements;
     const double sigma = 1.0 / (params.sigma_scale * h * h);
+    auto tb = std::chrono::steady_clock::now();
     std::vector<Piece> pieces = classify_dofs(*L.mapper);
+    t_cls += seconds_since(tb);
+    auto tc = std::chrono::steady_clock::now();
     L.pieces.resize(pieces.size());
     parallel_for(std::int64_t(pieces.size()), threads, [&](std::int64_t i) {
       Piece& pc = pieces[i];
@@ -478,8 +487,12 @@ Hierarchy::Hierarchy(const MultiPatchDomain& domain, int degree, int n0, int lev
           break;
       }
     });
+    t_pay += seconds_since(tc);
   }
   t_setup_ = seconds_since(t0);
+  if (timing)
+    std::fprintf(stderr, "[pmg setup] DofMapper %.2f s, classify_dofs %.2f s, piece payloads %.2f s (of %.2f s)\n", t_map,
+                 t_cls, t_pay, t_setup_);
 
   auto t1 = std::chrono::steady_clock::now();
   const int O = band_offsets(d, degree);
@@ -539,7 +552,10 @@ Hierarchy::Hierarchy(const MultiPatchDomain& domain, int degree, int n0, int lev
     }
   }
   t_setup_ += seconds_since(t2);
+  if (timing) std::fprintf(stderr, "[pmg setup] coarse matrix + Cholesky %.2f s\n", seconds_since(t2));
+  auto t3 = std::chrono::steady_clock::now();
   rhs_ = assemble_rhs(*levels_.back().mapper, rhs, threads);
+  if (timing) std::fprintf(stderr, "[pmg setup] load vector %.2f s\n", seconds_since(t3));
 }
 
 // ============================================================ domains

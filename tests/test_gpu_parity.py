@@ -245,14 +245,20 @@ def test_line_sweep_matches_tma_half(dom, p, lv, n0, min_ext, monkeypatch):
     assert rel(out["1"][1], out["0"][1]) < 1e-10
 
 
-@pytest.mark.parametrize("ntc", ["3", "5", "9", "11"])
+@pytest.mark.parametrize("ntc", ["3", "5", "9", "11", "9,8", "11,8", "9,11", "11,11", "9,0", "11,0"])
 @pytest.mark.parametrize("dom,p,lv,n0", [("c2", 4, 5, 2), ("c4", 3, 3, 2), ("c3", 8, 5, 2), ("c1", 2, 6, 2)])
 def test_smooth_forced_fd_panels(dom, p, lv, n0, ntc, monkeypatch):
-    """Every fast-diagonalization column panel (fd_pass_dmma_kernel<NTC, 1>,
-    NTC = 3, 5, 9, 11 n-tiles of 8 columns; fd_pick_ntc chooses per level)
-    against the oracle's FastDiagonalSolver::solve path (tensor.cpp:132-140)
-    on every level; the bench's c2 finest level runs NTC = 9."""
-    monkeypatch.setenv("PMG_FD_NTC", ntc)
+    """Every fast-diagonalization kernel configuration (fd_pass_dmma_kernel
+    <NTC, NW>: NTC = 3, 5, 9, 11 n-tiles of 8 columns, NW = 4, 8 or 11 warps
+    of 8 rows; "NTC,0" the resident-factor kernel fd_pass_resident_kernel<NTC>
+    on every pass whose contraction fits; fd_pick_cfg chooses per level and
+    pass) against the oracle's
+    FastDiagonalSolver::solve path (tensor.cpp:132-140) on every level; the
+    bench's c2 finest level runs <11, 11>, c5's <9, 4>."""
+    if "," in ntc:
+        monkeypatch.setenv("PMG_FD_CFG", ntc)
+    else:
+        monkeypatch.setenv("PMG_FD_NTC", ntc)
     h = Hierarchy(dom, p, lv, n0=n0)
     b, o = GpuBackend(h), oracle.Oracle(h)
     for level in range(h.num_levels):
