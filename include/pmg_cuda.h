@@ -83,6 +83,14 @@ int pmg_ctx_info(pmg_ctx* ctx, int what, int64_t* out);
  * assembled on the device (PMG_BAND_ASSEMBLE) hands its stiffness to a host
  * consumer -- the CPU checker and baseline.  n = K_local (2p+1)^d (n+p)^d. */
 int pmg_band_download(pmg_ctx* ctx, int level, double* host, int64_t n);
+/* Assemble the finest-level load vector on the device (assemble_rhs,
+ * assembly.cpp:299-365, by sum factorization over the patch quadrature grid)
+ * into `out` as a DistributedVector: every local patch holds its own share,
+ * Dirichlet slots 0.  rhs_kind = a resolved PMGH_RHS_* source of pmg_host.h
+ * (1 one, 2 sine2d, 3 sine3d, 4 sine_pi, 5 random_nodes with `seed`, 6 zero).
+ * Needs pmg_hierarchy_desc.geometry.  The sum order differs from the host
+ * loop's element scatter, so entries agree to rounding, not bitwise. */
+int pmg_assemble_load(pmg_ctx* ctx, int rhs_kind, uint64_t seed, pmg_vec* out);
 /* Launch everything on this cudaStream_t from now on (NULL: the ctx stream). */
 int pmg_set_stream(pmg_ctx* ctx, void* stream);
 int pmg_synchronize(pmg_ctx* ctx);

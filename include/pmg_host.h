@@ -46,6 +46,10 @@ int pmgh_build_ex(const char* domain, int split, int degree, int n0, int levels,
 void pmgh_free(pmgh_hierarchy* h);
 const char* pmgh_last_error(void);
 
+/* The source PMGH_RHS_DEFAULT stands for on this domain (a PMGH_RHS_* value);
+ * other kinds are returned unchanged. */
+int pmgh_resolve_rhs_kind(const char* domain, int dim, int rhs_kind);
+
 /* Whole-hierarchy descriptor; pointers live as long as h. */
 int pmgh_describe(pmgh_hierarchy* h, pmg_hierarchy_desc* out);
 /* Finest-level load vector (num_dofs of the finest level). */

@@ -116,6 +116,7 @@ def host_lib():
         _sig(lib, "pmgh_set_rhs", C.c_int, [_vp, C.c_int, C.c_uint64, C.c_int])
         _sig(lib, "pmgh_seconds", C.c_double, [_vp, C.c_int])
         _sig(lib, "pmgh_stored_entries", C.c_int64, [C.c_int, C.c_int, C.c_int, C.c_int])
+        _sig(lib, "pmgh_resolve_rhs_kind", C.c_int, [C.c_char_p, C.c_int, C.c_int])
         _sig(lib, "pmgh_reps", C.c_int, [_vp, C.c_int, C.POINTER(_ip), C.POINTER(_ip), C.POINTER(_ip)])
         _sig(lib, "pmgh_interfaces", C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(_ip)])
         _sig(lib, "pmgh_rank_plan", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(PmghRankPlanView)])
@@ -139,7 +140,7 @@ CUDA_SYMBOLS = [
     "pmg_coarse_solve", "pmg_dot", "pmg_axpy", "pmg_xpay",
     "pmg_mg_cycle", "pmg_precondition", "pmg_pcg_solve_device", "pmg_pcg_solve",
     "pmg_kernel_stats", "pmg_synchronize", "pmg_profile", "pmg_profile_read",
-    "pmg_band_download",
+    "pmg_band_download", "pmg_assemble_load",
     "pmg_nccl_unique_id", "pmg_hub_create", "pmg_hub_destroy", "pmg_hub_poison", "pmg_comm_bytes",
 ]
 
@@ -167,6 +168,7 @@ def cuda_lib():
         _sig(lib, "pmg_ctx_info", C.c_int, [_vp, C.c_int, C.POINTER(C.c_int64)])
         _sig(lib, "pmg_set_stream", C.c_int, [_vp, _vp])
         _sig(lib, "pmg_band_download", C.c_int, [_vp, C.c_int, _dp, C.c_int64])
+        _sig(lib, "pmg_assemble_load", C.c_int, [_vp, C.c_int, C.c_uint64, _vp])
         _sig(lib, "pmg_vec_create", C.c_int, [_vp, C.c_int, C.POINTER(_vp)])
         _sig(lib, "pmg_vec_free", None, [_vp])
         _sig(lib, "pmg_vec_upload", C.c_int, [_vp, _vp, C.c_int, _dp, C.c_int64])

@@ -114,6 +114,23 @@ class GpuBackend:
         self._check(self._lib.pmg_ctx_info(self._ctx, 5, C.byref(n)))
         return n.value / 1e6
 
+    def load_seconds(self) -> float:
+        """Wall time spent in assemble_load (device load-vector assembly)."""
+        n = C.c_int64()
+        self._check(self._lib.pmg_ctx_info(self._ctx, 7, C.byref(n)))
+        return n.value / 1e6
+
+    def assemble_load(self, rhs: str = "default", seed: int | None = None) -> DistVec:
+        """The finest-level load vector assembled on the device from the patch
+        geometry (pmg_assemble_load; assemble_rhs, assembly.cpp:299-365) as a
+        DistributedVector.  rhs = a source name of Hierarchy (\"default\": the
+        domain's own); seed defaults to the hierarchy's."""
+        from .hierarchy import RHS_KINDS
+        kind = N.host_lib().pmgh_resolve_rhs_kind(self.h.domain.encode(), self.h.dim, RHS_KINDS[rhs])
+        v = DistVec(self, self.h.finest_level)
+        self._check(self._lib.pmg_assemble_load(self._ctx, kind, self.h.seed if seed is None else seed, v._h))
+        return v
+
     def download_band(self, level: int) -> np.ndarray:
         """The level's operator as held on the device, as the reference's
         index-free full band [K_local][(2p+1)^d][(n+p)^d] (pmg_band_download)."""

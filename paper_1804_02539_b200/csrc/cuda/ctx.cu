@@ -76,6 +76,7 @@ struct DevLevel {
   FdPiece* d_int = nullptr;
   int n_int = 0;
   int4* int_items[6] = {};
+  unsigned* int_queue[6] = {};  // resident-factor passes: strip counters (kernels_fd.cu)
   int n_int_items[6] = {};
   int int_ntc[6] = {};  // kernel configuration per pass (fd_pick_cfg)
   std::vector<std::array<int, 3>> int_dims;  // host copy for flop counts
@@ -88,6 +89,7 @@ struct DevLevel {
   int* face_iface = nullptr;  // face piece dofs as interface indices
   long long face_ndof = 0;
   int4* face_items[4] = {};
+  unsigned* face_queue[4] = {};
   int n_face_items[4] = {};
   int face_ntc[4] = {};
   // edges / vertices
@@ -157,6 +159,10 @@ struct pmg_ctx {
   size_t bytes = 0;
   long long launches = 0, spmv_launches = 0;
   double assembly_seconds = 0.0;  // device stiffness assembly (PMG_BAND_ASSEMBLE levels)
+  double load_seconds = 0.0;      // device load-vector assembly (pmg_assemble_load)
+  // the patch geometry, copied when the descriptor carries it (pmg_assemble_load)
+  std::vector<pmg_patch_geometry> geo;
+  std::vector<std::vector<double>> geo_ctrl;
   std::string err;
   // live event timing (pmg_profile)
   bool profiling = false;
@@ -798,7 +804,8 @@ void build_level_rest(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
   // CTA work items of every pass.  Pieces with the same dims and the same
   // factor for the pass form a group whose rows are concatenated (no per-piece
   // row padding); items = (first piece, row panel, column panel, group rows).
-  auto make_items = [&](const std::vector<FdPiece>& ps, int naxes, int4** items, int* counts, int* ntcs) {
+  auto make_items = [&](const std::vector<FdPiece>& ps, int naxes, int4** items, int* counts, int* ntcs,
+                        unsigned** queues) {
     for (int pass = 0; pass < 2 * naxes; ++pass) {
       const int axis = pass % naxes, dir = pass / naxes;
       std::vector<std::pair<int, int>> groups;  // (first, count)
@@ -837,6 +844,8 @@ void build_level_rest(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
           gl.push_back({gr.first, rows});
         }
         fd_resident_items(gl, it);
+        queues[pass] = c.alloc<unsigned>(gl.size() + 1);
+        ck(cudaMemsetAsync(queues[pass], 0, sizeof(unsigned) * (gl.size() + 1), c.stream), "memset");
       }
       for (const auto& gr : groups) {
         if (fd_cfg_resident(cfg)) break;
@@ -851,8 +860,8 @@ void build_level_rest(pmg_ctx& c, const pmg_hierarchy_desc& D, int l) {
       ntcs[pass] = cfg;
     }
   };
-  make_items(h_int, d, L.int_items, L.n_int_items, L.int_ntc);
-  if (d == 3) make_items(h_face, 2, L.face_items, L.n_face_items, L.face_ntc);
+  make_items(h_int, d, L.int_items, L.n_int_items, L.int_ntc, L.int_queue);
+  if (d == 3) make_items(h_face, 2, L.face_items, L.n_face_items, L.face_ntc, L.face_queue);
 
   // ---- two-scale factor (TransferOperator ctor, transfer.cpp:10-19)
   if (l >= 1) {
@@ -927,6 +936,16 @@ void build_ctx(pmg_ctx& c, const pmg_hierarchy_desc& D) {
   if (D.num_levels < 2) throw PmgError(PMG_ERR_CONFIG, "need at least one refinement level");
   if (D.params.nu < 1 || D.params.mu < 1 || D.params.mu > 2) throw PmgError(PMG_ERR_CONFIG, "bad cycle parameters");
   c.lv.resize(c.nl);
+  if (D.geometry) {
+    c.geo.assign(D.geometry, D.geometry + D.num_patches);
+    c.geo_ctrl.resize(D.num_patches);
+    for (int k = 0; k < D.num_patches; ++k) {
+      size_t n = D.dim;
+      for (int a = 0; a < D.dim; ++a) n *= size_t(c.geo[k].elements[a] + c.geo[k].degree[a]);
+      c.geo_ctrl[k].assign(D.geometry[k].ctrl, D.geometry[k].ctrl + n);
+      c.geo[k].ctrl = c.geo_ctrl[k].data();
+    }
+  }
   fd_configure();
   size_t work_n = 1, tbuf_n = 1, face_n = 1;
   for (int l = 0; l < c.nl; ++l) {
@@ -1160,7 +1179,7 @@ void op_smooth(pmg_ctx& c, int l, const double* r, double* out, bool add, double
     TimedScope ts(c, 1, l, fd_pass_flops(L, L.int_dims, d, pass));
     launch_fd_pass(c.stream, L.d_int, L.int_items[pass], L.n_int_items[pass], L.int_ntc[pass], pass, d, in_mode,
                    out_mode, r, out,
-                   alpha, c.work[(pass + 1) & 1], c.work[pass & 1]);
+                   alpha, c.work[(pass + 1) & 1], c.work[pass & 1], L.int_queue[pass]);
     if (L.n_int_items[pass]) c.launches++;
   }
   if (fork) ck(cudaStreamWaitEvent(main, c.ev_join, 0), "cudaStreamWaitEvent");
@@ -1189,7 +1208,7 @@ void op_smooth_iface(pmg_ctx& c, int l, const double* r, double* out, bool add, 
         const int out_mode = pass == 1 ? FD_OUT_WORK_DIAG : FD_OUT_WORK;
         launch_fd_pass(c.stream, L.d_face, L.face_items[pass], L.n_face_items[pass], L.face_ntc[pass], pass, 2,
                        FD_IN_WORK, out_mode,
-                       nullptr, nullptr, 0.0, c.face_buf[(pass + 1) & 1], c.face_buf[pass & 1]);
+                       nullptr, nullptr, 0.0, c.face_buf[(pass + 1) & 1], c.face_buf[pass & 1], L.face_queue[pass]);
         c.launches++;
       }
     }
@@ -1733,8 +1752,23 @@ int pmg_ctx_info(pmg_ctx* ctx, int what, int64_t* out) {
       case 3: *out = ctx->lv[level].N; break;
       case 4: *out = ctx->pe - ctx->pb; break;
       case 5: *out = int64_t(ctx->assembly_seconds * 1e6); break;
+      case 7: *out = int64_t(ctx->load_seconds * 1e6); break;
       case 6: *out = ctx->comm ? int64_t(ctx->comm->calls) : 0; break;
       default: throw PmgError(PMG_ERR_CONFIG, "unknown info query");
+    }
+  });
+}
+
+int pmg_assemble_load(pmg_ctx* ctx, int rhs_kind, uint64_t seed, pmg_vec* out) {
+  return guarded(ctx, [&] {
+    check_vec(ctx, out, ctx->nl - 1);
+    need(!ctx->geo.empty(), PMG_ERR_CONFIG, "load vector assembly needs the patch geometry (desc.geometry)");
+    const DevLevel& L = ctx->lv[ctx->nl - 1];
+    try {
+      ctx->load_seconds += assemble_load_device(ctx->stream, ctx->dim, ctx->degree, L.n, ctx->geo.data(), ctx->pb,
+                                                L.K, rhs_kind, seed, L.l2g, out->d);
+    } catch (const AssemblyError& e) {
+      throw PmgError(PMG_ERR_GEOMETRY, e.what());
     }
   });
 }

@@ -98,6 +98,11 @@ struct AssemblyError : std::runtime_error {
 double assemble_level_device(cudaStream_t s, int dim, int degree, int elements, const pmg_patch_geometry* geo,
                              int patch_begin, int K, double* band, long long Sp, int Ob);
 
+// Load vector (assemble_rhs, assembly.cpp:299-365) of the local patches as a
+// distributed lattice vector [K][ext^d]; kind = a resolved PMGH_RHS_* source.
+double assemble_load_device(cudaStream_t s, int dim, int degree, int elements, const pmg_patch_geometry* geo,
+                            int patch_begin, int K, int kind, unsigned long long seed, const int* l2g, double* out);
+
 // ---------------------------------------------------------------- FD
 struct FdPiece {
   int dims[3];
@@ -120,11 +125,12 @@ enum FdOut { FD_OUT_WORK = 0, FD_OUT_WORK_DIAG = 1, FD_OUT_LATTICE_SET = 2, FD_O
 // strips) of the CTA (fd_pick_cfg)
 void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int cfg, int pass,
                     int naxes, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
-                    const double* work_in, double* work_out);
+                    const double* work_in, double* work_out, unsigned* queue = nullptr);
 int fd_pick_cfg(const long long* cols, const long long* weight, int n);
 bool fd_cfg_valid(int cfg);
 // cfg | kFdResident: the resident-factor kernel for short contractions
-// (K = N <= 88, many rows); its items come from fd_resident_items
+// (K = N <= 88, many rows); its items come from fd_resident_items, and each
+// items list needs its own zeroed strip counters: one unsigned per group + 1
 constexpr int kFdResident = 1 << 16;
 bool fd_cfg_resident(int cfg);
 void fd_resident_items(const std::vector<std::pair<int, long long>>& groups, std::vector<int4>& items);

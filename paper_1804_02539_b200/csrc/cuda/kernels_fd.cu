@@ -281,14 +281,17 @@ __global__ void __launch_bounds__(32 * NW, MINB) fd_pass_dmma_kernel(const FdPie
 // ---------------------------------------------------------------- short contractions
 // Passes with K = N <= 8 NTC (the 3D levels: c4/c5 contract 65-67 entries):
 // the factor stays resident.  One persistent CTA per SM loads B once; each of
-// its kResWarps warps then works alone -- it takes the next 8-row strip of
-// the CTA's range from a shared counter, copies the strip's X rows into its
-// own double buffer with cp.async while the previous strip multiplies, runs
-// ceil(K / 4) k-steps of NTC DMMAs from shared memory, and stores.  No
-// CTA-wide barrier after the prologue, no per-tile pipeline fill.
-// item = (first piece of the group, first strip, end strip, rows of the
-// group): the CTAs of a group split its strips evenly (fd_resident_items).
-constexpr int kResWarps = 12;
+// its NW warps then works alone -- it takes the next 8-row strip of its
+// group from a global counter (so every CTA of a group ends together: with
+// static ranges the slowest SM ran 20% behind the average), copies the
+// strip's X rows into its own double buffer with cp.async while the previous
+// strip multiplies, runs ceil(K / 4) k-steps of NTC DMMAs from shared memory,
+// and stores.  No CTA-wide barrier after the prologue, no per-tile pipeline
+// fill.  item = (first piece of the group, group index, number of groups,
+// rows of the group); queue = one strip counter per group, then the count of
+// finished CTAs: the last CTA to finish zeroes the counters for the next
+// launch (fd_resident_items shares the SMs out over the groups).
+constexpr int kResWarps = 12;  // the strip threshold of fd_pick_cfg
 
 // Row of a group as a warp lane sees it: the piece it lies in, its row there,
 // and where that row's input starts / its output goes.  All patch-local
@@ -301,18 +304,18 @@ struct ResRow {
   const double* aux;  // diagonal (FD_OUT_WORK_DIAG) or nothing
 };
 
-template <int NTC>
-__global__ void __launch_bounds__(32 * kResWarps, 1) fd_pass_resident_kernel(
-    const FdPiece* __restrict__ pieces, const int4* __restrict__ items, int pass, int naxes, int in_mode,
-    int out_mode, const double* __restrict__ lat_in, double* __restrict__ lat_out, double alpha,
-    const double* __restrict__ work_in, double* __restrict__ work_out) {
+template <int NTC, int NW>
+__global__ void __launch_bounds__(32 * NW, 1) fd_pass_resident_kernel(
+    const FdPiece* __restrict__ pieces, const int4* __restrict__ items, unsigned* __restrict__ queue, int pass,
+    int naxes, int in_mode, int out_mode, const double* __restrict__ lat_in, double* __restrict__ lat_out,
+    double alpha, const double* __restrict__ work_in, double* __restrict__ work_out) {
   PMG_PDL_ENTRY();
   constexpr int BN = 8 * NTC;
   constexpr int BS = (BN + 11) / 16 * 16 + 4;  // = 4 mod 16: conflict-free B fragments
   extern __shared__ __align__(16) double fd_smem[];
-  __shared__ int next_strip;
   const int4 it = items[blockIdx.x];
   const FdPiece& P0 = pieces[it.x];
+  unsigned* const next_strip = queue + it.y;
   const int axis = pass % naxes, dir = pass / naxes;
   const int K = P0.dims[axis];
   const int N = K;
@@ -321,17 +324,17 @@ __global__ void __launch_bounds__(32 * kResWarps, 1) fd_pass_resident_kernel(
   const int XS = (Kp & 7) == 4 ? Kp : Kp + 4;  // = 4 mod 8: conflict-free A fragments
   const int R = int(P0.total / K);             // rows per piece
   const int rows = it.w;
+  const int nstrips = (rows + 7) / 8;
   const int m0 = P0.dims[0], m1 = P0.dims[1];
   const int ext = P0.ext, ext2 = P0.ext * P0.ext;
   const int ostride = out_mode >= FD_OUT_LATTICE_SET ? (naxes == 3 ? ext2 : ext) : R;  // output column stride
   const double* __restrict__ B = P0.B[axis][dir];
   double* Bs = fd_smem;                 // [Kp][BS], zero outside K x N
-  double* Xall = Bs + (size_t)Kp * BS;  // [kResWarps][2][8][XS]
+  double* Xall = Bs + (size_t)Kp * BS;  // [NW][2][8][XS]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
 
-  if (tid == 0) next_strip = it.y;
-  for (int idx = tid; idx < Kp * BS; idx += 32 * kResWarps) {
+  for (int idx = tid; idx < Kp * BS; idx += 32 * NW) {
     const int kk = idx / BS, nn = idx - kk * BS;
     const bool ok = kk < K && nn < N;
     cp_async8(Bs + idx, ok ? B + kk * N + nn : B, ok);
@@ -370,20 +373,21 @@ __global__ void __launch_bounds__(32 * kResWarps, 1) fd_pass_resident_kernel(
     for (int k = t; k < K; k += 4, dst += 4, src += 4) cp_async8(dst, src, true);
   };
   auto grab = [&]() {
-    int s = 0;
-    if (lane == 0) s = atomicAdd(&next_strip, 1);
-    return __shfl_sync(0xffffffffu, s, 0);
+    unsigned s = 0;
+    if (lane == 0) s = atomicAdd(next_strip, 1u);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    return s < unsigned(nstrips) ? int(s) : nstrips;
   };
 
   int cur = grab();
-  ResRow wc = locate(cur < it.z ? cur : it.y);
-  if (cur < it.z) issue(wc, Xw);
+  ResRow wc = locate(cur < nstrips ? cur : 0);
+  if (cur < nstrips) issue(wc, Xw);
   cp_async_commit();
   int buf = 0;
-  while (cur < it.z) {
+  while (cur < nstrips) {
     const int nxt = grab();
     ResRow wn = wc;
-    if (nxt < it.z) {
+    if (nxt < nstrips) {
       wn = locate(nxt);
       issue(wn, Xw + (buf ^ 1) * 8 * XS);
     }
@@ -474,15 +478,25 @@ __global__ void __launch_bounds__(32 * kResWarps, 1) fd_pass_resident_kernel(
     buf ^= 1;
   }
   cp_async_wait<0>();
+  // every warp of this CTA has taken its last strip: the last CTA of the
+  // launch re-arms the counters (the next launch is ordered after this grid)
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned ngroups = unsigned(it.z);
+    if (atomicInc(queue + ngroups, gridDim.x - 1) == gridDim.x - 1)
+      for (unsigned q = 0; q < ngroups; ++q) queue[q] = 0u;
+  }
 }
 
-template <int NTC>
+template <int NTC, int NW>
 size_t fd_resident_smem(int K) {
   const int Kp = (K + 3) / 4 * 4;
   const int XS = (Kp & 7) == 4 ? Kp : Kp + 4;
   const int BS = (8 * NTC + 11) / 16 * 16 + 4;
-  return sizeof(double) * (size_t(Kp) * BS + size_t(kResWarps) * 2 * 8 * XS);
+  return sizeof(double) * (size_t(Kp) * BS + size_t(NW) * 2 * 8 * XS);
 }
+// warps per CTA: 16 with the 72-column panel (203 KB), 12 with 88 columns
+constexpr int kResWarps9 = 16, kResWarps11 = 12;
 
 // ---------------------------------------------------------------- small pieces
 // Pieces that fit in shared memory (coarse levels): one CTA runs the whole
@@ -705,8 +719,8 @@ void fd_configure() {
   ensure_smem((const void*)fd_pass_dmma_kernel<NT, NW, ST, MB>, FdTile<NT, NW, ST>::smem);
   PMG_FD_CONFIGS(PMG_FD_ATTR)
 #undef PMG_FD_ATTR
-  ensure_smem((const void*)fd_pass_resident_kernel<9>, fd_resident_smem<9>(72));
-  ensure_smem((const void*)fd_pass_resident_kernel<11>, fd_resident_smem<11>(88));
+  ensure_smem((const void*)fd_pass_resident_kernel<9, kResWarps9>, fd_resident_smem<9, kResWarps9>(72));
+  ensure_smem((const void*)fd_pass_resident_kernel<11, kResWarps11>, fd_resident_smem<11, kResWarps11>(88));
 }
 
 // CTA items of the resident-factor kernel: the SMs are shared out over the
@@ -742,8 +756,7 @@ void fd_resident_items(const std::vector<std::pair<int, long long>>& groups, std
     const long long strips = (groups[i].second + 7) / 8;
     const int nc = int(std::min<long long>(ctas[i], strips));
     for (int j = 0; j < nc; ++j)
-      items.push_back(make_int4(groups[i].first, int(strips * j / nc), int(strips * (j + 1) / nc),
-                                int(groups[i].second)));
+      items.push_back(make_int4(groups[i].first, int(i), int(groups.size()), int(groups[i].second)));
   }
 }
 
@@ -790,7 +803,7 @@ int fd_pick_cfg(const long long* cols, const long long* weight, int n) {
       kmax = std::max<long long>(kmax, cols[i]);
       strips += (weight[i] + 7) / 8;
     }
-    if (res_ok && kmax <= 88 && kmax >= 24 && strips >= 2LL * sms * kResWarps && n <= sms)
+    if (res_ok && kmax <= 88 && kmax >= 24 && strips >= 4LL * sms * kResWarps && n <= sms)
       return (kmax <= 72 ? 9 : 11) | kFdResident;
   }
   // large passes (every SM gets a full 88-row tile and the contraction is
@@ -850,16 +863,19 @@ int fd_pick_cfg(const long long* cols, const long long* weight, int n) {
 
 void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, int nitems, int cfg, int pass,
                     int naxes, int in_mode, int out_mode, const double* lat_in, double* lat_out, double alpha,
-                    const double* work_in, double* work_out) {
+                    const double* work_in, double* work_out, unsigned* queue) {
   if (nitems == 0) return;
   if (fd_cfg_resident(cfg)) {
     // one smem size per launch: the largest contraction the kernel may see is 8 NTC
+    if (!queue) throw std::runtime_error("FD pass: the resident-factor kernel needs its strip counters");
     if ((cfg & 255) == 9) {
-      launch_k(fd_pass_resident_kernel<9>, dim3(nitems), dim3(32 * kResWarps), fd_resident_smem<9>(72), s, pieces,
-               items, pass, naxes, in_mode, out_mode, lat_in, lat_out, alpha, work_in, work_out);
+      launch_k(fd_pass_resident_kernel<9, kResWarps9>, dim3(nitems), dim3(32 * kResWarps9),
+               fd_resident_smem<9, kResWarps9>(72), s, pieces, items, queue, pass, naxes, in_mode, out_mode, lat_in,
+               lat_out, alpha, work_in, work_out);
     } else {
-      launch_k(fd_pass_resident_kernel<11>, dim3(nitems), dim3(32 * kResWarps), fd_resident_smem<11>(88), s, pieces,
-               items, pass, naxes, in_mode, out_mode, lat_in, lat_out, alpha, work_in, work_out);
+      launch_k(fd_pass_resident_kernel<11, kResWarps11>, dim3(nitems), dim3(32 * kResWarps11),
+               fd_resident_smem<11, kResWarps11>(88), s, pieces, items, queue, pass, naxes, in_mode, out_mode, lat_in,
+               lat_out, alpha, work_in, work_out);
     }
     return;
   }

@@ -207,6 +207,10 @@ __global__ void coarse_scatter_kernel(const int* __restrict__ l2g, long long n, 
 // mode 0: out = s; 1: out = s on non-Dirichlet slots, 0 elsewhere (last
 // restriction pass); 2: out += coef s on non-Dirichlet slots (last
 // prolongation pass, u += c P coarse).
+// IDX = the index type of the element arithmetic: 32-bit whenever the
+// vectors have < 2^31 entries (three 64-bit divisions per output made the
+// pass instruction-bound: c5's finest transfers ran at 0.2 of their bytes).
+template <typename IDX>
 __global__ void ts_axis_kernel(TsDev ts, int transpose, int K, int d, int in0, int in1, int in2, int axis,
                                const double* __restrict__ in, double* __restrict__ out, int mode,
                                const int* __restrict__ l2g, double coef) {
@@ -214,27 +218,30 @@ __global__ void ts_axis_kernel(TsDev ts, int transpose, int K, int d, int in0, i
   int dims_in[3] = {in0, in1, in2};
   int dims_out[3] = {in0, in1, in2};
   dims_out[axis] = transpose ? ts.coarse_dim : ts.fine_dim;
-  long long inner = 1, outer = 1;
+  IDX inner = 1, outer = 1;
   for (int a = 0; a < axis; ++a) inner *= dims_in[a];
   for (int a = axis + 1; a < d; ++a) outer *= dims_in[a];
   const int m_in = dims_in[axis], m_out = dims_out[axis];
-  const long long per_in = inner * m_in * outer, per_out = inner * m_out * outer;
-  const long long total = per_out * K;
-  for (long long idx = blockIdx.x * (long long)kThreads + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * kThreads) {
-    const long long k = idx / per_out;
-    const long long rem = idx - k * per_out;
-    const long long t = rem % inner;
-    const int j = int((rem / inner) % m_out);
-    const long long o = rem / (inner * m_out);
+  const IDX per_in = inner * m_in * outer, per_out = inner * m_out * outer;
+  const IDX total = per_out * K;
+  const IDX slab = inner * m_out;
+  for (IDX idx = blockIdx.x * IDX(kThreads) + threadIdx.x; idx < total; idx += IDX(gridDim.x) * kThreads) {
+    const IDX k = idx / per_out;
+    const IDX rem = idx - k * per_out;
+    const IDX o = rem / slab;
+    const IDX rs = rem - o * slab;
+    const int j = int(rs / inner);
+    const IDX t = rs - IDX(j) * inner;
     const double* src = in + k * per_in + o * inner * m_in + t;
     double s = 0.0;
     if (!transpose) {
       const double* v = ts.vals + ts.row_off[j];
       const int st = ts.row_start[j];
-      for (int q = 0; q < ts.row_len[j]; ++q) s = fma(v[q], src[(long long)(st + q) * inner], s);
+      const int len = ts.row_len[j];
+      for (int q = 0; q < len; ++q) s = fma(v[q], src[IDX(st + q) * inner], s);
     } else {
-      for (int q = ts.col_off[j]; q < ts.col_off[j + 1]; ++q) s = fma(ts.col_val[q], src[(long long)ts.col_row[q] * inner], s);
+      const int q1 = ts.col_off[j + 1];
+      for (int q = ts.col_off[j]; q < q1; ++q) s = fma(ts.col_val[q], src[IDX(ts.col_row[q]) * inner], s);
     }
     if (mode == 0)
       out[idx] = s;
@@ -641,8 +648,15 @@ void launch_ts_axis(cudaStream_t s, const TsDev& ts, bool transpose, int K, int 
   const long long total = per_out * K;
   long long g = (total + kThreads - 1) / kThreads;
   if (g > 148LL * 32) g = 148LL * 32;
-  launch_k(ts_axis_kernel, dim3(int(g < 1 ? 1 : g)), dim3(kThreads), 0, s, ts, transpose ? 1 : 0, K, d, in_dims[0], in_dims[1],
-                                                         d == 3 ? in_dims[2] : 1, axis, in, out, mode, l2g, coef);
+  long long per_in = 1;
+  for (int a = 0; a < d; ++a) per_in *= in_dims[a];
+  const bool small = total < (1LL << 30) && per_in * K < (1LL << 30);
+  if (small)
+    launch_k(ts_axis_kernel<unsigned>, dim3(int(g < 1 ? 1 : g)), dim3(kThreads), 0, s, ts, transpose ? 1 : 0, K, d,
+             in_dims[0], in_dims[1], d == 3 ? in_dims[2] : 1, axis, in, out, mode, l2g, coef);
+  else
+    launch_k(ts_axis_kernel<long long>, dim3(int(g < 1 ? 1 : g)), dim3(kThreads), 0, s, ts, transpose ? 1 : 0, K, d,
+             in_dims[0], in_dims[1], d == 3 ? in_dims[2] : 1, axis, in, out, mode, l2g, coef);
 }
 void launch_iface_partial(cudaStream_t s, int n, const int* rep_off, const int* rep_slot, const double* r,
                           double* tloc) {

@@ -62,17 +62,16 @@ int guarded(F&& f) {
   }
 }
 
+int resolve_rhs_kind(const std::string& domain, int dim, int kind) {
+  if (kind != PMGH_RHS_DEFAULT) return kind;
+  if (domain == "c1") return PMGH_RHS_SINE_PI;
+  if (domain.size() == 2 && domain[0] == 'c') return PMGH_RHS_RANDOM_NODES;
+  if (domain.rfind("jitter(", 0) == 0) return PMGH_RHS_RANDOM_NODES;
+  return dim == 2 ? PMGH_RHS_SINE2D : PMGH_RHS_SINE3D;
+}
+
 RhsSpec rhs_spec(const std::string& domain, int dim, int kind, std::uint64_t seed) {
-  if (kind == PMGH_RHS_DEFAULT) {
-    if (domain == "c1")
-      kind = PMGH_RHS_SINE_PI;
-    else if (domain.size() == 2 && domain[0] == 'c')
-      kind = PMGH_RHS_RANDOM_NODES;
-    else if (domain.rfind("jitter(", 0) == 0)
-      kind = PMGH_RHS_RANDOM_NODES;
-    else
-      kind = dim == 2 ? PMGH_RHS_SINE2D : PMGH_RHS_SINE3D;
-  }
+  kind = resolve_rhs_kind(domain, dim, kind);
   RhsSpec s;
   s.seed = seed;
   switch (kind) {
@@ -81,6 +80,7 @@ RhsSpec rhs_spec(const std::string& domain, int dim, int kind, std::uint64_t see
       break;
     case PMGH_RHS_ZERO:
       s.f = [](const double*) { return 0.0; };
+      s.zero = true;  // no quadrature loop: the load vector comes from elsewhere (pmg_assemble_load)
       break;
     case PMGH_RHS_SINE2D:  // harness.cpp:28-30
       s.f = [](const double* x) { return 50.0 * M_PI * M_PI * std::sin(5 * M_PI * x[0]) * std::sin(5 * M_PI * x[1]); };
@@ -238,6 +238,10 @@ int pmgh_build_ex(const char* domain, int split, int degree, int n0, int levels,
 }
 
 void pmgh_free(pmgh_hierarchy* h) { delete h; }
+
+int pmgh_resolve_rhs_kind(const char* domain, int dim, int rhs_kind) {
+  return resolve_rhs_kind(domain ? domain : "", dim, rhs_kind);
+}
 
 int pmgh_describe(pmgh_hierarchy* H, pmg_hierarchy_desc* out) {
   if (!H || !out) return fail(PMG_ERR_CONFIG, "pmgh_describe: null argument");

@@ -297,6 +297,7 @@ std::vector<double> assemble_rhs(const DofMapper& mapper, const RhsSpec& spec, i
   const int q1 = int(rule.nodes.size());
   const BasisTables tab = tabulate(p, n, rule);
   const int K = dom.num_patches();
+  if (spec.zero) return std::vector<double>(std::size_t(mapper.num_dofs()), 0.0);
   std::int64_t ecount = 1, nq = 1;
   for (int a = 0; a < d; ++a) {
     ecount *= n;

@@ -73,6 +73,7 @@ struct RhsSpec {
   enum Kind { function, random_nodes } kind = function;
   std::function<double(const double*)> f;
   std::uint64_t seed = 42;
+  bool zero = false;  // f == 0: assemble_rhs returns zeros without the quadrature loop
 };
 
 class Hierarchy {
