@@ -113,6 +113,7 @@ struct FdPiece {
   long long work_off;  // offset in the work buffers
   const double* B[3][2];  // [axis][0 fwd: B(k,n)=V(k,n) | 1 bwd: B(k,n)=V(n,k)], row-major k*N+n
   const double* diag;     // total, original (axis 0 fastest) layout
+  const double* rdiag;    // 1 / diag (correctly rounded on the host): the resident-factor kernel multiplies
 };
 
 enum FdIn { FD_IN_WORK = 0, FD_IN_LATTICE = 1 };

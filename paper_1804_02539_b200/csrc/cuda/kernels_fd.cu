@@ -301,7 +301,7 @@ constexpr int kResWarps = 12;  // the strip threshold of fd_pick_cfg
 struct ResRow {
   const double* src;  // first input element of the row
   double* dst;        // output element (row, column 0)
-  const double* aux;  // diagonal (FD_OUT_WORK_DIAG) or nothing
+  const double* aux;  // reciprocal diagonal of the row (FD_OUT_WORK_DIAG)
 };
 
 template <int NTC, int NW>
@@ -364,28 +364,43 @@ __global__ void __launch_bounds__(32 * NW, 1) fd_pass_resident_kernel(
     } else {
       w.dst = work_out + P.work_off + rl;
     }
-    w.aux = P.diag + rl;
+    w.aux = P.rdiag + rl;
     return w;
   };
   auto issue = [&](const ResRow& w, double* xb) {
     double* dst = xb + g * XS + t;
     const double* src = w.src + t;
-    for (int k = t; k < K; k += 4, dst += 4, src += 4) cp_async8(dst, src, true);
+    int k = t;
+#pragma unroll 1
+    for (; k + 12 < K; k += 16, dst += 16, src += 16) {
+      cp_async8(dst, src, true);
+      cp_async8(dst + 4, src + 4, true);
+      cp_async8(dst + 8, src + 8, true);
+      cp_async8(dst + 12, src + 12, true);
+    }
+    for (; k < K; k += 4, dst += 4, src += 4) cp_async8(dst, src, true);
   };
-  auto grab = [&]() {
-    unsigned s = 0;
-    if (lane == 0) s = atomicAdd(next_strip, 1u);
-    s = __shfl_sync(0xffffffffu, s, 0);
+  // lane 0 takes strips from the group's counter two ahead: the atomic's
+  // round trip (about 1 us) is over before its result is broadcast
+  unsigned pending = 0;
+  auto request = [&]() {
+    if (lane == 0) pending = atomicAdd(next_strip, 1u);
+  };
+  auto take = [&]() {
+    const unsigned s = __shfl_sync(0xffffffffu, pending, 0);
     return s < unsigned(nstrips) ? int(s) : nstrips;
   };
 
-  int cur = grab();
+  request();
+  int cur = take();
+  request();
   ResRow wc = locate(cur < nstrips ? cur : 0);
   if (cur < nstrips) issue(wc, Xw);
   cp_async_commit();
   int buf = 0;
   while (cur < nstrips) {
-    const int nxt = grab();
+    const int nxt = take();
+    request();
     ResRow wn = wc;
     if (nxt < nstrips) {
       wn = locate(nxt);
@@ -432,42 +447,46 @@ __global__ void __launch_bounds__(32 * NW, 1) fd_pass_resident_kernel(
       for (int j = 0; j < NTC; ++j) dmma(acc[j][0], acc[j][1], a0, b0[j]);
     }
     if (cur * 8 + g < rows) {
-      // Y(row, n) at dst + ostride n, n = 8 j + 2 t + i
-      double* o = wc.dst + (long long)ostride * (2 * t);
+      // Y(row, n) at dst + ostride n, n = 8 j + 2 t + i: two running pointers
+      // (columns n and n + 1) stepped by 8 columns, so the per-element address
+      // arithmetic is two 64-bit adds per j
       const long long step = (long long)ostride * 8;
+      double* o0 = wc.dst + (long long)ostride * (2 * t);
+      double* o1 = o0 + ostride;
+      const int nrem = N - 2 * t;  // column n = 8 j + 2 t is valid iff 8 j < nrem
       if (out_mode == FD_OUT_WORK) {
 #pragma unroll
-        for (int j = 0; j < NTC; ++j, o += step) {
-          const int n = 8 * j + 2 * t;
-          if (n < N) o[0] = acc[j][0];
-          if (n + 1 < N) o[ostride] = acc[j][1];
+        for (int j = 0; j < NTC; ++j, o0 += step, o1 += step) {
+          if (8 * j < nrem) *o0 = acc[j][0];
+          if (8 * j + 1 < nrem) *o1 = acc[j][1];
         }
       } else if (out_mode == FD_OUT_LATTICE_SET) {
 #pragma unroll
-        for (int j = 0; j < NTC; ++j, o += step) {
-          const int n = 8 * j + 2 * t;
-          if (n < N) o[0] = alpha * acc[j][0];
-          if (n + 1 < N) o[ostride] = alpha * acc[j][1];
+        for (int j = 0; j < NTC; ++j, o0 += step, o1 += step) {
+          if (8 * j < nrem) *o0 = alpha * acc[j][0];
+          if (8 * j + 1 < nrem) *o1 = alpha * acc[j][1];
         }
       } else {
         // all loads first (one round trip), then the stores
-        const double* q = (out_mode == FD_OUT_WORK_DIAG ? wc.aux : wc.dst) + (long long)ostride * (2 * t);
+        const double* q0 = (out_mode == FD_OUT_WORK_DIAG ? wc.aux : wc.dst) + (long long)ostride * (2 * t);
+        const double* q1 = q0 + ostride;
         double ld[NTC][2];
 #pragma unroll
-        for (int j = 0; j < NTC; ++j) {
-          const int n = 8 * j + 2 * t;
-          ld[j][0] = n < N ? q[step * j] : 1.0;
-          ld[j][1] = n + 1 < N ? q[step * j + ostride] : 1.0;
+        for (int j = 0; j < NTC; ++j, q0 += step, q1 += step) {
+          ld[j][0] = 8 * j < nrem ? *q0 : 1.0;
+          ld[j][1] = 8 * j + 1 < nrem ? *q1 : 1.0;
         }
+        if (out_mode == FD_OUT_WORK_DIAG) {  // ld = 1 / diag
 #pragma unroll
-        for (int j = 0; j < NTC; ++j, o += step) {
-          const int n = 8 * j + 2 * t;
-          if (out_mode == FD_OUT_WORK_DIAG) {
-            if (n < N) o[0] = acc[j][0] / ld[j][0];
-            if (n + 1 < N) o[ostride] = acc[j][1] / ld[j][1];
-          } else {
-            if (n < N) o[0] = ld[j][0] + alpha * acc[j][0];
-            if (n + 1 < N) o[ostride] = ld[j][1] + alpha * acc[j][1];
+          for (int j = 0; j < NTC; ++j, o0 += step, o1 += step) {
+            if (8 * j < nrem) *o0 = acc[j][0] * ld[j][0];
+            if (8 * j + 1 < nrem) *o1 = acc[j][1] * ld[j][1];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < NTC; ++j, o0 += step, o1 += step) {
+            if (8 * j < nrem) *o0 = fma(alpha, acc[j][0], ld[j][0]);
+            if (8 * j + 1 < nrem) *o1 = fma(alpha, acc[j][1], ld[j][1]);
           }
         }
       }
