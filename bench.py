@@ -363,7 +363,7 @@ def main():
     t0 = time.perf_counter()
     # with device assembly the load vector is assembled on the device as well
     # (pmg_assemble_load): the host quadrature loop is 13 s at c4, 50 s at c5
-    device_load = assembly == "device" and world == 1
+    device_load = assembly == "device"
     h = build_hierarchy(args, world=world, threads=threads, assembly=assembly,
                         rhs="zero" if device_load else "default")
     t_setup = time.perf_counter() - t0
@@ -382,7 +382,11 @@ def main():
     b.set_stream(stream.cuda_stream)
     if device_load:
         f_dev = b.assemble_load("default")
-        f_host = b.gather_global(L, f_dev)
+        f_host = b.gather_global(L, f_dev)  # replica sums of this rank's patches
+        if dist is not None:  # the global load vector: the sum over the ranks' shares
+            t = torch.from_numpy(f_host).cuda()
+            dist.all_reduce(t)
+            f_host = t.cpu().numpy()
     else:
         f_host = h.rhs()
         f_dev = b.to_distributed_owner(L, f_host)

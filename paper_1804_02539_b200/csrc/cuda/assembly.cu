@@ -229,6 +229,8 @@ inline void ckA(cudaError_t e, const char* what) {
 
 }  // namespace
 
+namespace {
+
 // ---------------------------------------------------------------- load vector
 // assemble_rhs (assembly.cpp:299-365) by sum factorization: the source term
 // times w |det J| on the patch's tensor quadrature grid, then one contraction
@@ -335,6 +337,8 @@ __global__ void load_contract_kernel(AsmDims A, const double* __restrict__ T, co
   if (l2g) s = l2g[idx] >= 0 ? s : 0.0;
   dst[idx] = s;
 }
+
+}  // namespace
 
 double assemble_level_device(cudaStream_t s, int dim, int degree, int elements, const pmg_patch_geometry* geo,
                              int patch_begin, int K, double* band, long long Sp, int Ob) {

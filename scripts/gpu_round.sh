@@ -8,8 +8,10 @@ set -u
 mkdir -p gpurun_out
 TAG=${TAG:-round}
 nvidia-smi -L; nproc
-python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/tests_$TAG.log 2>&1
-echo "tests rc=$?"; tail -3 gpurun_out/tests_$TAG.log
+if [ "${SKIP_TESTS:-0}" != 1 ]; then
+  python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/tests_$TAG.log 2>&1
+  echo "tests rc=$?"; tail -3 gpurun_out/tests_$TAG.log
+fi
 python bench.py > gpurun_out/bench_c5_$TAG.json 2> gpurun_out/bench_c5_$TAG.err; echo "c5 rc=$?"
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_c5_$TAG.json 2> gpurun_out/bench_ref_c5_$TAG.err; echo "ref rc=$?"
 for c in c4 c2 c1 c3p2 c3p3 c3p4 c3p6 c3p8; do
@@ -32,9 +34,10 @@ P
 # profiles: each capture only after the plain command above exited 0
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5_$TAG.csv \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/launches_c5_$TAG.log 2>&1; echo "launch list rc=$?"
-cap() { # name, kernel regex, count, bench args
-  ncu --set full --clock-control none --import-source on -k "regex:$2" -c $3 -o gpurun_out/prof_$1_$TAG \
+cap() { # name, kernel regex, count, bench args.  gpurun brings back <= 64 MiB: keep the raw metric page, not the report
+  ncu --set full --clock-control none --import-source on -k "regex:$2" -c $3 -o /tmp/prof_$1_$TAG -f \
     python bench.py $4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_$1_$TAG.log 2>&1; echo "ncu $1 rc=$?"
+  ncu -i /tmp/prof_$1_$TAG.ncu-rep --page raw --csv > gpurun_out/ncu_raw_$1_$TAG.csv 2>/dev/null
 }
 cap sweep3d_c5 spmv_sweep3d 1 "--config c5"
 cap fdres_c5 fd_pass_resident 6 "--config c5"

@@ -1,7 +1,7 @@
 """Summarise one ncu report (--set full) as JSON and keep its raw metric page
 as CSV (text, instead of committing the binary .ncu-rep):
 
-  python scripts/ncu_report.py rep.ncu-rep out.json [raw.csv] [key=value ...]
+  python scripts/ncu_report.py rep.ncu-rep|raw.csv out.json [raw.csv] [key=value ...]
 
 One JSON entry per captured launch: duration, launch shape, DRAM bytes,
 pipe / SM activity and the warp-stall profile; key=value pairs are added to
@@ -47,8 +47,11 @@ def main():
     rep, out = sys.argv[1], sys.argv[2]
     raw_out = sys.argv[3] if len(sys.argv) > 3 and "=" not in sys.argv[3] else None
     extra = dict(a.split("=", 1) for a in sys.argv[3:] if "=" in a)
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    if raw_out:
+    if rep.endswith(".csv"):  # an exported raw page (ncu -i rep --page raw --csv)
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if raw_out and raw_out != rep:
         open(raw_out, "w").write(raw)
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]

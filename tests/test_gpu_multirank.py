@@ -97,3 +97,35 @@ def test_concurrent_line_sweeps(R, monkeypatch):
     u, rep, _ = parallel_pcg_solve(h, R, f)
     assert rep.iterations == len(hist_ref) - 1
     assert np.abs(u - u_ref).max() <= 1e-10 * np.abs(u_ref).max()
+
+
+@pytest.mark.parametrize("dom,p,lv,n0,rhs", [("c3", 4, 4, 2, "default"), ("unit_grid(2,2,2)", 2, 3, 2, "sine3d")])
+@pytest.mark.parametrize("R", [2, 4])
+def test_matrix_free_and_device_load_on_ranks(dom, p, lv, n0, rhs, R):
+    """Round-2 paths on R ranks: the Kronecker operator (PMG_BAND_KRONECKER)
+    applies each rank's patches with that rank's geometry factors, and
+    pmg_assemble_load assembles each rank's share of the load vector (the
+    seeded node values indexed by the global patch number).  The shares sum to
+    the host vector; the solve has the serial iteration count and solution."""
+    h = Hierarchy(dom, p, lv, n0=n0, rhs=rhs, operator="kronecker")
+    o = oracle.Oracle(h)
+    L = h.finest_level
+    f = h.rhs()
+    u_ref, hist_ref, _, _ = o.pcg_solve(f)
+    x = rand(h.num_dofs(L), 3)
+    ref_ax = o.apply_op(L, x)
+
+    def body(r, b):
+        fd = b.assemble_load(rhs)
+        share = b.gather_global(L, fd)
+        ax = b.gather_global(L, b.apply_op(L, b.to_accumulated(L, x)))
+        u, rep = b.pcg_solve_device(fd)
+        return share, ax, b.gather_global(L, u), rep.iterations
+
+    out = run_ranks(h, R, body)
+    assert np.abs(sum(o_[0] for o_ in out) - f).max() <= 1e-13 * np.abs(f).max()
+    assert np.abs(sum(o_[1] for o_ in out) - ref_ax).max() <= 1e-13 * np.abs(ref_ax).max()
+    for r, (_, _, u, its) in enumerate(out):
+        m = local_dof_mask(h, L, r, R)
+        assert its == len(hist_ref) - 1
+        assert np.abs(u[m] - u_ref[m]).max() <= 1e-10 * np.abs(u_ref).max()
