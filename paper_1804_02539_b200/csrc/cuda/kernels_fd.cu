@@ -515,7 +515,8 @@ size_t fd_resident_smem(int K) {
   return sizeof(double) * (size_t(Kp) * BS + size_t(NW) * 2 * 8 * XS);
 }
 // warps per CTA: 16 with the 72-column panel (203 KB), 12 with 88 columns
-constexpr int kResWarps9 = 16, kResWarps11 = 12;
+// (8 for passes with few strips per warp: c4's finest level has 4290 strips)
+constexpr int kResWarps9 = 16, kResWarps9s = 8, kResWarps11 = 12;
 
 // ---------------------------------------------------------------- small pieces
 // Pieces that fit in shared memory (coarse levels): one CTA runs the whole
@@ -739,6 +740,7 @@ void fd_configure() {
   PMG_FD_CONFIGS(PMG_FD_ATTR)
 #undef PMG_FD_ATTR
   ensure_smem((const void*)fd_pass_resident_kernel<9, kResWarps9>, fd_resident_smem<9, kResWarps9>(72));
+  ensure_smem((const void*)fd_pass_resident_kernel<9, kResWarps9s>, fd_resident_smem<9, kResWarps9s>(72));
   ensure_smem((const void*)fd_pass_resident_kernel<11, kResWarps11>, fd_resident_smem<11, kResWarps11>(88));
 }
 
@@ -785,7 +787,10 @@ int fd_cfg_rows(int cfg) { return 8 * ((cfg >> 8) & 255); }
 int fd_cfg_cols(int cfg) { return 8 * (cfg & 255); }
 
 bool fd_cfg_valid(int cfg) {
-  if (fd_cfg_resident(cfg)) return (cfg & 255) == 9 || (cfg & 255) == 11;
+  if (fd_cfg_resident(cfg)) {  // NTC | warps << 8 | kFdResident
+    const int ntc = cfg & 255, nw = (cfg >> 8) & 255;
+    return (ntc == 9 && (nw == kResWarps9 || nw == kResWarps9s)) || (ntc == 11 && nw == kResWarps11);
+  }
 #define PMG_FD_VALID(NT, NW, ST, MB) \
   if (cfg == (NT | NW << 8)) return true;
   PMG_FD_CONFIGS(PMG_FD_VALID)
@@ -802,8 +807,15 @@ int fd_pick_cfg(const long long* cols, const long long* weight, int n) {
       if (nw != 0) return ntc | nw << 8;
       // "ntc,0": the resident-factor kernel where the contraction fits, else the default
       int kmax = 0;
-      for (int i = 0; i < n; ++i) kmax = std::max<long long>(kmax, cols[i]);
-      if (kmax <= 8 * ntc && n <= 148) return ntc | kFdResident;
+      long long strips = 0;
+      for (int i = 0; i < n; ++i) {
+        kmax = std::max<long long>(kmax, cols[i]);
+        strips += (weight[i] + 7) / 8;
+      }
+      if (kmax <= 8 * ntc && n <= 148 && (ntc == 9 || ntc == 11)) {
+        const int rw = ntc == 11 ? kResWarps11 : strips >= 4LL * 148 * kResWarps ? kResWarps9 : kResWarps9s;
+        return ntc | rw << 8 | kFdResident;
+      }
     }
   }
   if (const char* e = std::getenv("PMG_FD_NTC")) return std::atoi(e) | 4 << 8;
@@ -822,8 +834,15 @@ int fd_pick_cfg(const long long* cols, const long long* weight, int n) {
       kmax = std::max<long long>(kmax, cols[i]);
       strips += (weight[i] + 7) / 8;
     }
-    if (res_ok && kmax <= 88 && kmax >= 24 && strips >= 4LL * sms * kResWarps && n <= sms)
-      return (kmax <= 72 ? 9 : 11) | kFdResident;
+    static const int small_ok = [] {  // experiments: PMG_FD_RES_SMALL=1 takes the 8-warp variant from 2 strips per warp
+      const char* e = std::getenv("PMG_FD_RES_SMALL");
+      return e && e[0] == '1';
+    }();
+    if (res_ok && kmax <= 88 && kmax >= 24 && n <= sms) {
+      if (strips >= 4LL * sms * kResWarps)
+        return kmax <= 72 ? (9 | kResWarps9 << 8 | kFdResident) : (11 | kResWarps11 << 8 | kFdResident);
+      if (small_ok && kmax <= 72 && strips >= 2LL * sms * kResWarps9s) return 9 | kResWarps9s << 8 | kFdResident;
+    }
   }
   // large passes (every SM gets a full 88-row tile and the contraction is
   // long enough to amortise the tile's fill and drain): one 11-warp CTA per
@@ -887,7 +906,11 @@ void launch_fd_pass(cudaStream_t s, const FdPiece* pieces, const int4* items, in
   if (fd_cfg_resident(cfg)) {
     // one smem size per launch: the largest contraction the kernel may see is 8 NTC
     if (!queue) throw std::runtime_error("FD pass: the resident-factor kernel needs its strip counters");
-    if ((cfg & 255) == 9) {
+    if ((cfg & 255) == 9 && ((cfg >> 8) & 255) == kResWarps9s) {
+      launch_k(fd_pass_resident_kernel<9, kResWarps9s>, dim3(nitems), dim3(32 * kResWarps9s),
+               fd_resident_smem<9, kResWarps9s>(72), s, pieces, items, queue, pass, naxes, in_mode, out_mode, lat_in,
+               lat_out, alpha, work_in, work_out);
+    } else if ((cfg & 255) == 9) {
       launch_k(fd_pass_resident_kernel<9, kResWarps9>, dim3(nitems), dim3(32 * kResWarps9),
                fd_resident_smem<9, kResWarps9>(72), s, pieces, items, queue, pass, naxes, in_mode, out_mode, lat_in,
                lat_out, alpha, work_in, work_out);
