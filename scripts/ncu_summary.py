@@ -1,9 +1,13 @@
 """Summarise an ncu --csv launch list (gpu__time_duration.sum per launch) by
 kernel name: total device time, share, launches, average.
 
-  python scripts/ncu_summary.py launches.csv
+  python scripts/ncu_summary.py launches.csv [exclude-regex]
+
+Kernels matching exclude-regex (setup: assembly, relayout ...) are left out of
+the totals and shares.
 """
 import csv
+import re
 import sys
 from collections import defaultdict
 
@@ -17,6 +21,8 @@ for r in rows:
     unit = r.get("Metric Unit", "ns")
     v *= {"ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1e-3)
     name = r["Kernel Name"]
+    if len(sys.argv) > 2 and re.search(sys.argv[2], name):
+        continue
     tot[name] += v
     cnt[name] += 1
 T = sum(tot.values())

@@ -55,8 +55,11 @@ for name in ("fdres_c5", "fdwide_c2", "kron_c3p8"):
     report(name)
 csv = out / f"launches_c5_{tag}.csv"
 if csv.exists():
-    txt = subprocess.run([sys.executable, str(ROOT / "scripts" / "ncu_summary.py"), str(csv)], capture_output=True,
-                         text=True).stdout
+    setup = "asm_|load_coeff|load_contract|zero_dirichlet|relayout|lattice_from_global|global_from_lattice"
+    txt = subprocess.run([sys.executable, str(ROOT / "scripts" / "ncu_summary.py"), str(csv), setup],
+                         capture_output=True, text=True).stdout
+    txt = "Solve-path kernels (setup kernels excluded):\n" + txt + "\nAll kernels:\n" + subprocess.run(
+        [sys.executable, str(ROOT / "scripts" / "ncu_summary.py"), str(csv)], capture_output=True, text=True).stdout
     (prof / f"launches_c5_{tag}.txt").write_text(
         "ncu --metrics gpu__time_duration.sum --clock-control none, python bench.py --steps 1 --warmup 3 "
         "--no-cpu-baseline (c5).\nThe device-loop solve graph has a conditional node, which ncu does not profile: the "

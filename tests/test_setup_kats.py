@@ -334,3 +334,36 @@ def test_device_assembly_descriptor():
     with pytest.raises(Exception):
         oracle.Oracle(h)
     assert h.assemble_seconds() < hh.assemble_seconds()
+
+
+def test_rhs_kind_resolution_and_zero_source():
+    """pmgh_resolve_rhs_kind names the source PMGH_RHS_DEFAULT stands for (what
+    pmg_assemble_load is given); the zero source skips the quadrature loop."""
+    from paper_1804_02539_b200 import _native as N
+    from paper_1804_02539_b200.hierarchy import RHS_KINDS
+    lib = N.host_lib()
+    assert lib.pmgh_resolve_rhs_kind(b"c1", 2, 0) == RHS_KINDS["sine_pi"]
+    for dom in (b"c2", b"c5", b"jitter(2,2,1)"):
+        assert lib.pmgh_resolve_rhs_kind(dom, 3, 0) == RHS_KINDS["random_nodes"]
+    assert lib.pmgh_resolve_rhs_kind(b"lshape", 2, 0) == RHS_KINDS["sine2d"]
+    assert lib.pmgh_resolve_rhs_kind(b"fichera", 3, 0) == RHS_KINDS["sine3d"]
+    assert lib.pmgh_resolve_rhs_kind(b"fichera", 3, RHS_KINDS["one"]) == RHS_KINDS["one"]
+    h = Hierarchy("c4", 3, 2, n0=2, rhs="zero")
+    assert h.rhs().shape == (h.num_dofs(h.finest_level),) and not h.rhs().any()
+
+
+def test_kronecker_levels_keep_the_host_band():
+    """operator='kronecker' marks levels >= 1 PMG_BAND_KRONECKER for the device
+    and leaves the assembled band in the descriptor for the CPU checker: the
+    oracle runs on it unchanged."""
+    from paper_1804_02539_b200 import _native as N
+    import oracle
+    hb = Hierarchy("c3", 3, 3, n0=2)
+    hk = Hierarchy("c3", 3, 3, n0=2, operator="kronecker")
+    assert hk.desc.levels[0].band_format == N.PMG_BAND_TENSOR
+    for level in range(1, hk.num_levels):
+        assert hk.desc.levels[level].band_format == N.PMG_BAND_KRONECKER
+        assert np.array_equal(hk.band(level), hb.band(level))
+    ub, hist_b, _, _ = oracle.Oracle(hb).pcg_solve(hb.rhs())
+    uk, hist_k, _, _ = oracle.Oracle(hk).pcg_solve(hk.rhs())
+    assert np.array_equal(ub, uk) and np.array_equal(hist_b, hist_k)
