@@ -9,7 +9,7 @@ mkdir -p gpurun_out
 TAG=${TAG:-round}
 nvidia-smi -L; nproc
 if [ "${SKIP_TESTS:-0}" != 1 ]; then
-  python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/tests_$TAG.log 2>&1
+  PMG_TEST_FULL=${PMG_TEST_FULL:-1} python -m pytest tests -m gpu -q -p no:cacheprovider --durations=25 > gpurun_out/tests_$TAG.log 2>&1
   echo "tests rc=$?"; tail -3 gpurun_out/tests_$TAG.log
 fi
 python bench.py > gpurun_out/bench_c5_$TAG.json 2> gpurun_out/bench_c5_$TAG.err; echo "c5 rc=$?"

@@ -116,3 +116,13 @@ def explicit_prolongation(h, level):
 
 def rand(n, seed):
     return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+# The driver runs `pytest -m gpu` under a 20-minute limit.  The default
+# selection keeps every BASELINE family at full size and every kernel
+# configuration; PMG_TEST_FULL=1 (scripts/gpu_round.sh) adds the remaining
+# combinations (all five c3 degrees at full size, every FD configuration on
+# every desk hierarchy, the full-c4 host-vs-device assembly comparison).
+import os  # noqa: E402
+
+FULL_MATRIX = os.environ.get("PMG_TEST_FULL") == "1"

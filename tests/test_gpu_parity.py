@@ -23,6 +23,7 @@ import pytest
 
 from paper_1804_02539_b200 import Hierarchy, baseline_hierarchy
 from paper_1804_02539_b200.backend import GpuBackend, mg_precondition, pcg_generic
+from tests.helpers import FULL_MATRIX
 
 import oracle
 
@@ -179,7 +180,9 @@ def test_pcg_matches_oracle(setup):
 
 @pytest.mark.parametrize("dom,p,lv,n0", [("c1", 2, 5, 2), ("c2", 4, 5, 2), ("c3", 1, 6, 2), ("c3", 5, 5, 2),
                                          ("c3", 8, 5, 2), ("c4", 3, 3, 2), ("fichera", 1, 6, 1),
-                                         ("fichera", 2, 5, 1), ("c5", 4, 3, 2)])
+                                         ("fichera", 2, 5, 1),
+                                         # 3D at p = 4 (host assembly: 4 min at c5 L3, PMG_TEST_FULL=1 only)
+                                         ("c5", 4, 3, 2) if FULL_MATRIX else ("c4", 4, 2, 2)])
 def test_half_band_matches_full_band(dom, p, lv, n0, monkeypatch):
     """The symmetric half band (default on TMA levels) against all O offsets
     (PMG_FULL_BAND=1): same operator up to the rounding asymmetry of the
@@ -245,31 +248,49 @@ def test_line_sweep_matches_tma_half(dom, p, lv, n0, min_ext, monkeypatch):
     assert rel(out["1"][1], out["0"][1]) < 1e-10
 
 
-@pytest.mark.parametrize("ntc", ["3", "5", "9", "11", "9,8", "11,8", "9,11", "11,11", "9,0", "11,0"])
-@pytest.mark.parametrize("dom,p,lv,n0", [("c2", 4, 5, 2), ("c4", 3, 3, 2), ("c3", 8, 5, 2), ("c1", 2, 6, 2)])
+FD_CONFIGS = ["3", "5", "9", "11", "9,8", "11,8", "9,11", "11,11", "9,0", "11,0"]
+# every configuration on a 2D and a 3D hierarchy; PMG_TEST_FULL=1 adds two more 2D ones
+FD_DOMAINS = [("c2", 4, 5, 2), ("c4", 3, 3, 2)] + ([("c3", 8, 5, 2), ("c1", 2, 6, 2)] if FULL_MATRIX else [])
+
+
+@pytest.mark.parametrize("ntc", FD_CONFIGS)
+@pytest.mark.parametrize("dom,p,lv,n0", FD_DOMAINS)
 def test_smooth_forced_fd_panels(dom, p, lv, n0, ntc, monkeypatch):
     """Every fast-diagonalization kernel configuration (fd_pass_dmma_kernel
     <NTC, NW>: NTC = 3, 5, 9, 11 n-tiles of 8 columns, NW = 4, 8 or 11 warps
     of 8 rows; "NTC,0" the resident-factor kernel fd_pass_resident_kernel<NTC>
     on every pass whose contraction fits; fd_pick_cfg chooses per level and
-    pass) against the oracle's
-    FastDiagonalSolver::solve path (tensor.cpp:132-140) on every level; the
-    bench's c2 finest level runs <11, 11>, c5's <9, 4>."""
+    pass) against the oracle's FastDiagonalSolver::solve path
+    (tensor.cpp:132-140) on every level; the bench's c2 finest level runs
+    <11, 11>, c5's the resident-factor kernel <9>."""
     if "," in ntc:
         monkeypatch.setenv("PMG_FD_CFG", ntc)
     else:
         monkeypatch.setenv("PMG_FD_NTC", ntc)
-    h = Hierarchy(dom, p, lv, n0=n0)
-    b, o = GpuBackend(h), oracle.Oracle(h)
+    h, o, smooth_ref, u_ref, hist_ref = _fd_reference(dom, p, lv, n0)
+    b = GpuBackend(h)
     for level in range(h.num_levels):
         r = rand(h.num_dofs(level), 61 + level)
         got = b.gather_global(level, b.smooth(level, b.to_distributed_owner(level, r)))
-        assert rel(got, o.smooth(level, r)) < 1e-12, level
-    f = h.rhs()
-    u_ref, hist_ref, _, _ = o.pcg_solve(f)
-    u, rep = b.pcg_solve(f)
+        assert rel(got, smooth_ref[level]) < 1e-12, level
+    u, rep = b.pcg_solve(h.rhs())
     assert rep.iterations == len(hist_ref) - 1
     assert rel(u, u_ref) < 1e-10
+
+
+_FD_REF = {}
+
+
+def _fd_reference(dom, p, lv, n0):
+    """Hierarchy and oracle results of one domain, shared by its configurations."""
+    key = (dom, p, lv, n0)
+    if key not in _FD_REF:
+        h = Hierarchy(dom, p, lv, n0=n0)
+        o = oracle.Oracle(h)
+        smooth_ref = [o.smooth(level, rand(h.num_dofs(level), 61 + level)) for level in range(h.num_levels)]
+        u_ref, hist_ref, _, _ = o.pcg_solve(h.rhs())
+        _FD_REF[key] = (h, o, smooth_ref, u_ref, hist_ref)
+    return _FD_REF[key]
 
 
 @pytest.mark.parametrize("dom,p,lv,n0", [("c2", 4, 5, 2), ("c4", 3, 3, 2), ("lshape", 2, 3, 1), ("c2", 4, 7, 2)])
@@ -347,7 +368,7 @@ def test_plane_sweep_matches_tma_half(dom, p, lv, n0, min_ext, monkeypatch):
 
 
 @pytest.mark.parametrize("dom,p,lv,n0,rhs", [("lshape", 2, 3, 1, "one"), ("c2", 4, 4, 2, "default"),
-                                             ("c4", 3, 3, 2, "default"), ("fichera", 2, 3, 1, "sine3d")])
+                                             ("c4", 3, 2, 2, "default"), ("fichera", 2, 3, 1, "sine3d")])
 @pytest.mark.parametrize("prm", [dict(mu=2), dict(nu=2), dict(mu=2, nu=2, damp_coarse=True), dict(tau=0.2)],
                          ids=["W", "V22", "W22damp", "tau"])
 def test_cycle_parameters_match_oracle(dom, p, lv, n0, rhs, prm):
